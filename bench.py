@@ -1,0 +1,417 @@
+"""Benchmark: time-to-solution of the reachability linear solve (Jacobi + BiCGStab) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
+
+Workload (BASELINE.json configs[1], "C2"): the reference generator's strictly diagonally
+dominant system n = 1e6, nnz = 1e7 (GenSpec(n=10**6, nnz=10**7, seed=trial_seed(0, 1e6,
+None, 1e7, 0)), bit-identical to mcreach.generate_dd_matrix) with rhs generate_rhs(n, seed).
+One step = one Jacobi solve + one BiCGStab solve from x0 = 0 to tol 1e-10, each including
+its final true residual. Metric value = solves per second over the whole job (N replicas at
+N > 1: the C2 system fits one GPU and does not shard, "replicas only" in DESIGN.md).
+
+Our arm: inputs resident in HBM (device-pointer C ABI), L2 flushed (512 MiB write) before
+every step, CUDA events on the stream the library launches on, barrier + synchronize around
+the timed loop, max over ranks. `e2e` repeats the step through the public API with HOST
+buffers (pinned): matrix upload + both solves + x back to the host, every step.
+`roofline` is the dominant kernel (the CSR SpMV tile kernel, k_spmv) timed alone with CUDA
+events (L2 flushed between launches) against its algorithmic bytes 12*nnz + 8*(n+1) + 16*n.
+`cpu_baseline` times the reference's own CPU path (mcreach jacobi-par + bicgstab-par,
+workers = all host cores) on one full solve pair, falling back to the C oracle port.
+`--impl reference` times the reference's CPU path alone, same metric and unit.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "time-to-solution & SpMV HBM GB/s (Jacobi/BiCGStab) at 1/2/4/8 B200 vs CPU"
+UNIT = "solves/s"
+FALLBACK_HBM_GBS = 6650.0
+
+
+# ----------------------------------------------------------------------------- workload
+
+def make_workload(config: str):
+    from paper_1210_6412_b200.generator import GenSpec, generate_dd_matrix, generate_rhs, trial_seed
+    if config == "c2":
+        n, nnz = 10 ** 6, 10 ** 7
+        seed = trial_seed(0, n, None, nnz, 0)
+        spec = GenSpec(n=n, nnz=nnz, seed=seed)
+        desc = ("C2: reference-generator DD system n=1e6, nnz=1e7 "
+                "(GenSpec(n=10**6, nnz=10**7, seed=trial_seed(0,1e6,None,1e7,0)))")
+    elif config == "c1":
+        n = 2000
+        seed = trial_seed(0, n, 0.1, None, 0)
+        spec = GenSpec(n=n, density=0.1, seed=seed)
+        desc = "C1: reference-generator DD system n=2000, density 0.1"
+    elif config == "c3":
+        n, seed = 16384, 3
+        spec = GenSpec(n=n, density=1.0, seed=seed)
+        desc = "C3: dense DD system n=16384 (dense slab storage)"
+    else:
+        raise SystemExit(f"unknown config {config}")
+    m = generate_dd_matrix(spec)
+    b = generate_rhs(spec.n, spec.seed)
+    return m, b, desc, spec
+
+
+def alg_bytes(n: int, nnz: int, nnz_off: int) -> dict:
+    """f64 values, int32 columns, int64 row pointers, x gathered once."""
+    spmv = 12 * nnz + 8 * (n + 1) + 16 * n
+    return {"spmv": spmv,
+            "jacobi_sweep": 12 * nnz_off + 8 * (n + 1) + 32 * n,
+            "bicgstab_iteration": 2 * (12 * nnz + 8 * (n + 1)) + 152 * n}
+
+
+def load_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def load_traffic(kernel_key: str):
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh)["kernels"][kernel_key]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """Samples SM clock + throttle reasons with NVML while the timed region runs."""
+
+    def __init__(self, index: int):
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self._ok = True
+        except Exception:
+            pass
+
+    _NAMES = {0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+              0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+              0x80: "hw_power_brake_slowdown"}
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self._nv.nvmlDeviceGetClockInfo(self._h, self._nv.NVML_CLOCK_SM))
+                r = self._nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for bit, name in self._NAMES.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        if self._ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._ok:
+            self._t.join(timeout=1)
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- CPU legs
+
+def reference_module():
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(os.path.join(ref, "mcreach")) and ref not in sys.path:
+        sys.path.append(ref)
+    try:
+        import mcreach  # noqa: F401
+        from mcreach import solvers as ms
+        return ms
+    except Exception:
+        return None
+
+
+def cpu_solve_pair(m, b, threads: int):
+    """One full Jacobi + BiCGStab solve pair of the reference's CPU path. Returns
+    (seconds, kind, iterations). kind 'reference' = mcreach itself (baseline/_ref),
+    'port' = the C restatement in oracle/ (when the reference is not installed)."""
+    ms = reference_module()
+    if ms is not None:
+        from mcreach import CsrMatrix as RefCsr
+        rm = RefCsr(m.n, m.rstart, m.col, m.nonzero)
+        cfg = ms.SolverConfig(workers=threads)
+        t0 = time.perf_counter()
+        jr = ms.SOLVERS["jacobi-par"](rm, b, cfg)
+        br = ms.SOLVERS["bicgstab-par"](rm, b, cfg)
+        return time.perf_counter() - t0, "reference", (jr.iterations, br.iterations)
+    from oracle import oracle
+    oracle.set_threads(threads)
+    t0 = time.perf_counter()
+    j = oracle.jacobi(m, b)
+    bb = oracle.bicgstab(m, b)
+    return time.perf_counter() - t0, "port", (j["iterations"], bb["iterations"])
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    m, b, desc, spec = make_workload(args.config)
+    threads = os.cpu_count() or 1
+    times = []
+    kind = None
+    iters = None
+    for i in range(args.warmup + args.steps):
+        dt, kind, iters = cpu_solve_pair(m, b, threads)
+        if i >= args.warmup:
+            times.append(dt)
+    total = sum(times)
+    value = 2 * len(times) / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / len(times), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: reference generator, bit-identical inputs",
+        "config": {"workload": desc, "n": spec.n, "nnz": int(m.m), "tolerance": 1e-10,
+                   "solve_pair": "jacobi-par + bicgstab-par", "parallelism": "cpu threads"},
+        "iterations": {"jacobi": iters[0], "bicgstab": iters[1]},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": f"full C2 solve pair per step ({'mcreach' if kind == 'reference' else 'oracle C port'}, {threads} threads)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- GPU arm
+
+def run_ours(args):
+    import ctypes
+
+    import numpy as np
+    import torch
+
+    from paper_1210_6412_b200 import _lib
+    from paper_1210_6412_b200.solvers import DeviceMatrix
+    from paper_1210_6412_b200.sparse import CsrMatrix
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    L = _lib.load()
+
+    m, b, desc, spec = make_workload(args.config)
+    n, nnz = int(m.n), int(m.m)
+    nnz_off = nnz - int(np.count_nonzero(np.repeat(np.arange(n), np.diff(m.rstart)) == m.col))
+    ab = alg_bytes(n, nnz, nnz_off)
+    stream = torch.cuda.Stream(dev)  # a real stream: the legacy default stream (0) cannot be handed over
+    torch.cuda.set_stream(stream)
+
+    dm = DeviceMatrix(m, local)
+    L.mcr_set_stream(dm.handle, ctypes.c_void_p(stream.cuda_stream))
+    L.mcr_set_dot_mode(dm.handle, _lib.DOTS_TREE)
+    b_dev = torch.from_numpy(b).to(dev)
+    x_dev = torch.empty(n, dtype=torch.float64, device=dev)
+    y_dev = torch.empty(n, dtype=torch.float64, device=dev)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
+
+    def solve(fn):
+        rep = _lib.Report()
+        rc = fn(dm.handle, ctypes.c_void_p(b_dev.data_ptr()), None, 1e-10, 10_000,
+                ctypes.c_void_p(x_dev.data_ptr()), ctypes.byref(rep))
+        if rc not in (_lib.MCR_OK, _lib.MCR_NOT_CONVERGED):
+            raise RuntimeError(f"solve failed rc={rc}: {_lib.last_error()}")
+        return rep
+
+    def step():
+        rj = solve(L.mcr_jacobi_device)
+        rb = solve(L.mcr_bicgstab_device)
+        return rj, rb
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    step_ms, jac_ms, bic_ms = [], [], []
+    launches = 0
+    reps = None
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            rj, rb = step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+            jac_ms.append(rj.device_seconds * 1e3)
+            bic_ms.append(rb.device_seconds * 1e3)
+            launches += rj.kernel_launches + rb.kernel_launches
+            reps = (rj, rb)
+    torch.cuda.synchronize()
+    total_ms = sum(step_ms)
+    if dist:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        dist.barrier()
+    value = 2.0 * world * args.steps / (total_ms / 1e3)
+
+    # ---- dominant kernel alone: CSR SpMV (k_spmv) with CUDA events, L2 flushed
+    spmv_ms = []
+    xin = torch.rand(n, dtype=torch.float64, device=dev)
+    for i in range(args.warmup + max(args.steps, 10)):
+        flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        L.mcr_matvec_device(dm.handle, ctypes.c_void_p(xin.data_ptr()),
+                            ctypes.c_void_p(y_dev.data_ptr()))
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if i >= args.warmup:
+            spmv_ms.append(e0.elapsed_time(e1))
+    spmv_s = statistics.mean(spmv_ms) / 1e3
+    peak, peak_src = load_peak()
+    achieved = ab["spmv"] / spmv_s / 1e9
+    traffic = load_traffic("k_spmv<EPI_Y>")
+
+    # ---- end to end through the public API with pinned host buffers
+    def pinned(a):
+        t = torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+        return t, t.numpy()
+
+    _rs_t, rs_h = pinned(m.rstart)
+    _col_t, col_h = pinned(m.col)
+    _val_t, val_h = pinned(m.nonzero)
+    _b_t, b_h = pinned(b)
+    _x_t, x_h = pinned(np.zeros(n))
+    hm = CsrMatrix(n, rs_h, col_h, val_h)
+    e2e_s = []
+    for i in range(args.warmup + args.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        h = DeviceMatrix(hm, local)             # H2D: rowptr, col, val
+        for method in ("jacobi", "bicgstab"):   # H2D: b; D2H: x
+            fn = L.mcr_jacobi if method == "jacobi" else L.mcr_bicgstab
+            rep = _lib.Report()
+            rc = fn(h.handle, ctypes.c_void_p(b_h.ctypes.data), None, 1e-10, 10_000,
+                    ctypes.c_void_p(x_h.ctypes.data), ctypes.byref(rep))
+            assert rc in (_lib.MCR_OK, _lib.MCR_NOT_CONVERGED), _lib.last_error()
+        h.close()
+        torch.cuda.synchronize()
+        if i >= args.warmup:
+            e2e_s.append(time.perf_counter() - t0)
+    e2e_total = sum(e2e_s)
+    if dist:
+        t = torch.tensor([e2e_total], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_total = float(t.item())
+    e2e_value = 2.0 * world * args.steps / e2e_total
+    h2d = 8 * (n + 1) + 8 * nnz + 8 * nnz + 2 * 8 * n
+    d2h = 2 * 8 * n
+
+    # ---- CPU baseline (rank 0, N = 1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        dt, kind, iters = cpu_solve_pair(m, b, threads)
+        cpu = {"value": 2.0 / dt, "unit": UNIT, "cores": threads, "kind": kind,
+               "sample": f"one full C2 solve pair (jacobi {iters[0]} sweeps + bicgstab "
+                         f"{iters[1]} iterations) by {'mcreach jacobi-par/bicgstab-par' if kind == 'reference' else 'the oracle C port'}, {threads} threads, {dt:.1f} s"}
+
+    rj, rb = reps
+    jac_it, bic_it = int(rj.iterations), int(rb.iterations)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: reference generator (bit-identical to mcreach.generate_dd_matrix)",
+        "config": {"workload": desc, "n": n, "nnz": nnz, "tolerance": 1e-10,
+                   "solve_pair": "jacobi + bicgstab (tree dots) from x0=0",
+                   "l2": "flushed before every step (512 MiB write); SpMV working set 144 MB",
+                   "parallelism": f"replicas x{world}"},
+        "time_to_solution_ms": {"jacobi": statistics.median(jac_ms),
+                                "bicgstab": statistics.median(bic_ms)},
+        "iterations": {"jacobi": jac_it, "bicgstab": bic_it},
+        "per_iteration": {
+            "jacobi_sweep_us": 1e3 * statistics.median(jac_ms) / max(jac_it, 1),
+            "jacobi_sweep_gbs": ab["jacobi_sweep"] * jac_it / (statistics.median(jac_ms) / 1e3) / 1e9,
+            "bicgstab_iteration_us": 1e3 * statistics.median(bic_ms) / max(bic_it, 1),
+            "bicgstab_iteration_gbs": ab["bicgstab_iteration"] * bic_it / (statistics.median(bic_ms) / 1e3) / 1e9,
+        },
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "k_spmv<EPI_Y> (CSR SpMV, one launch = one full M x)",
+                     "algorithmic_bytes": ab["spmv"], "launch_us": spmv_s * 1e6,
+                     "peak_source": peak_src},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h,
+                "note": "public API per step: DeviceMatrix upload + mcr_jacobi + mcr_bicgstab (pinned host b/x) + destroy"},
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+    }
+    if cpu:
+        line["cpu_baseline"] = cpu
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,145 @@
+/*
+ * mcr.h -- C ABI of the B200-native reachability solver (libmcr.so, sm_100a).
+ *
+ * Drop-in boundary for the solve path of the reference package `mcreach`
+ * (/root/reference/pkg/src/mcreach). Every entry point takes plain pointers and sizes;
+ * no C++ or torch type crosses it. Host-pointer entry points copy inputs to the device and
+ * the result back (what a Python/ctypes caller uses); `*_device` entry points take device
+ * pointers on the handle's GPU (inputs already resident in HBM).
+ *
+ * Reference interface each entry point replaces (file:line in /root/reference/pkg/src/mcreach):
+ *   mcr_matrix_create   CsrMatrix + its cached scipy handle      sparse.py:71-98
+ *                       diagonal() / _jacobi_diagonal()          sparse.py:194-198, solvers.py:277-282
+ *                       without_diagonal() (built lazily)        sparse.py:227-231
+ *   mcr_matvec          matvec(a, x)                             sparse.py:184-191
+ *   mcr_residual_inf    residual_inf_norm(m, x, b)               solvers.py:123-133
+ *   mcr_jacobi          jacobi_solve(m, b, config)               solvers.py:194-230
+ *   mcr_bicgstab        bicgstab_solve(m, b, config)             solvers.py:399-426, 450-491
+ *   status codes        ZeroDiagonal / NotConverged / Breakdown  solvers.py:43-78
+ *
+ * Thread safety: calls on one handle are serialised by a per-handle mutex; different handles
+ * may be used concurrently. The library owns all device memory of a handle.
+ */
+#ifndef MCR_H
+#define MCR_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define MCR_API __attribute__((visibility("default")))
+#else
+#define MCR_API
+#endif
+
+/* Return codes (the Python wrapper maps them onto the reference's exceptions). */
+enum {
+    MCR_OK = 0,                /* converged; outputs filled                                  */
+    MCR_NOT_CONVERGED = 1,     /* NotConverged: outputs hold the last iterate                */
+    MCR_BREAKDOWN = 2,         /* Breakdown: outputs hold the snapshot before that iteration */
+    MCR_ZERO_DIAGONAL = 3,     /* ZeroDiagonal: report->zero_diagonal_index                  */
+    MCR_DIMENSION = 4,         /* malformed CSR / mismatched sizes                           */
+    MCR_CUDA_ERROR = 5,        /* CUDA failure; see mcr_last_error()                         */
+    MCR_INVALID_ARGUMENT = 6
+};
+
+/* Breakdown.which of the reference (solvers.py:465-480). */
+enum { MCR_BD_NONE = 0, MCR_BD_Y_PREV_W = 1, MCR_BD_Q_V = 2, MCR_BD_T_T = 3 };
+
+/* Device storage selection for mcr_matrix_create. AUTO picks dense 32-row slabs when the
+ * matrix is at least 2/3 full and n >= 1024; otherwise CSR, laid out as SELL-32-sigma when the
+ * caller asks for it (coalesced thread-per-row streaming) and as CSR tiles staged by
+ * TMA bulk copies otherwise (the default). SELL / TILES force one CSR layout. mcr_matrix_info reports the
+ * layout in use (DENSE, SELL or TILES). */
+enum {
+    MCR_STORAGE_AUTO = 0,
+    MCR_STORAGE_CSR = 1,
+    MCR_STORAGE_DENSE = 2,
+    MCR_STORAGE_SELL = 3,
+    MCR_STORAGE_TILES = 4
+};
+
+typedef struct mcr_matrix mcr_matrix;
+
+/* Outcome of one solve; field meaning follows SolveResult (solvers.py:112-120). */
+typedef struct mcr_report {
+    int64_t iterations;          /* sweeps / iterations (breakdown: the breakdown iteration) */
+    int32_t converged;
+    int32_t breakdown_which;     /* MCR_BD_*                                                 */
+    int64_t breakdown_iteration;
+    int64_t zero_diagonal_index; /* first row without a non-zero stored diagonal, else -1   */
+    double residual_inf;         /* max|b - M x| with the full M                             */
+    double device_seconds;       /* CUDA-event time: iteration loop + final residual         */
+    int64_t kernel_launches;     /* kernels launched by this call                            */
+} mcr_report;
+
+typedef struct mcr_matrix_info {
+    int64_t n;
+    int64_t nnz;
+    int32_t storage;             /* MCR_STORAGE_DENSE, MCR_STORAGE_SELL or MCR_STORAGE_TILES */
+    int32_t device;
+    int64_t tiles;               /* CSR row tiles                                           */
+    int64_t max_row_nnz;
+    int64_t first_zero_diagonal; /* -1 when every row has a non-zero diagonal               */
+    int64_t device_bytes;        /* bytes of device memory held by the handle               */
+} mcr_matrix_info;
+
+/* Library version (major*10000 + minor*100 + patch). */
+MCR_API int mcr_version(void);
+
+/* Number of visible CUDA devices (0 on a machine without a GPU). */
+MCR_API int mcr_device_count(int* count);
+
+/* Upload an n x n CSR matrix (host arrays, int64 row starts and columns, float64 values,
+ * rows sorted by column) to `device`. The caller keeps ownership of the host arrays. */
+MCR_API int mcr_matrix_create(int64_t n, const int64_t* rstart, const int64_t* col,
+                              const double* nonzero, int device, int storage,
+                              mcr_matrix** out);
+MCR_API void mcr_matrix_destroy(mcr_matrix* m);
+MCR_API int mcr_matrix_info_get(const mcr_matrix* m, mcr_matrix_info* info);
+
+/* Inner products of BiCGStab: TREE (default) = deterministic fixed-shape tree reductions,
+ * fused into the producing kernels; SEQUENTIAL = the reference's strictly left-to-right
+ * _dot_ascending (solvers.py:136-141), bit-identical to the reference and much slower (one
+ * dependent add per element). Jacobi, SpMV and the residual are bit-identical in both modes. */
+enum { MCR_DOTS_TREE = 0, MCR_DOTS_SEQUENTIAL = 1 };
+MCR_API int mcr_set_dot_mode(mcr_matrix* m, int mode);
+
+/* Use `stream` (a cudaStream_t on the handle's device, or NULL for the handle's own stream)
+ * for every later call on this handle. */
+MCR_API int mcr_set_stream(mcr_matrix* m, void* stream);
+
+/* y = M x, each row summed in ascending column order, no FMA (bit-identical to scipy). */
+MCR_API int mcr_matvec(mcr_matrix* m, const double* x, double* y);
+MCR_API int mcr_matvec_device(mcr_matrix* m, const double* d_x, double* d_y);
+
+/* max|b - M x| (NaN-propagating, like numpy max). */
+MCR_API int mcr_residual_inf(mcr_matrix* m, const double* x, const double* b, double* out);
+
+/* Jacobi: x' = (b - R x) / diag(M) from the frozen previous iterate; stop when
+ * max|x' - x| <= tol (the count includes the certifying sweep). x0 may be NULL (zeros). */
+MCR_API int mcr_jacobi(mcr_matrix* m, const double* b, const double* x0, double tol,
+                       int64_t max_iterations, double* x_out, mcr_report* report);
+MCR_API int mcr_jacobi_device(mcr_matrix* m, const double* d_b, const double* d_x0,
+                              double tol, int64_t max_iterations, double* d_x_out,
+                              mcr_report* report);
+
+/* Un-preconditioned BiCGStab with shadow vector q = r0; converged when max|s| <= tol
+ * (tested before the final x/r update, which is still applied). */
+MCR_API int mcr_bicgstab(mcr_matrix* m, const double* b, const double* x0, double tol,
+                         int64_t max_iterations, double* x_out, mcr_report* report);
+MCR_API int mcr_bicgstab_device(mcr_matrix* m, const double* d_b, const double* d_x0,
+                                double tol, int64_t max_iterations, double* d_x_out,
+                                mcr_report* report);
+
+/* Message of the last failing call on this thread ("" if none). */
+MCR_API const char* mcr_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MCR_H */

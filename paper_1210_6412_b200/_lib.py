@@ -1,0 +1,110 @@
+"""ctypes binding of libmcr.so (include/mcr.h).
+
+The shared library is the only compute path: if it is missing or cannot be loaded, every
+solver call raises ``NativeLibraryError``; there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.environ.get("MCR_LIB") or os.path.join(_HERE, "libmcr.so")
+
+MCR_OK = 0
+MCR_NOT_CONVERGED = 1
+MCR_BREAKDOWN = 2
+MCR_ZERO_DIAGONAL = 3
+MCR_DIMENSION = 4
+MCR_CUDA_ERROR = 5
+MCR_INVALID_ARGUMENT = 6
+
+STORAGE_AUTO, STORAGE_CSR, STORAGE_DENSE, STORAGE_SELL, STORAGE_TILES = 0, 1, 2, 3, 4
+BREAKDOWN_NAMES = {1: "y_prev*w", 2: "q*v", 3: "t*t"}
+
+EXPORTS = (
+    "mcr_version", "mcr_device_count", "mcr_matrix_create", "mcr_matrix_destroy",
+    "mcr_matrix_info_get", "mcr_set_stream", "mcr_matvec", "mcr_matvec_device",
+    "mcr_residual_inf", "mcr_jacobi", "mcr_jacobi_device", "mcr_bicgstab",
+    "mcr_bicgstab_device", "mcr_last_error", "mcr_set_dot_mode",
+)
+DOTS_TREE, DOTS_SEQUENTIAL = 0, 1
+
+
+class NativeLibraryError(RuntimeError):
+    """libmcr.so is missing, failed to load, or a CUDA call inside it failed."""
+
+
+class Report(ctypes.Structure):
+    _fields_ = [
+        ("iterations", ctypes.c_int64),
+        ("converged", ctypes.c_int32),
+        ("breakdown_which", ctypes.c_int32),
+        ("breakdown_iteration", ctypes.c_int64),
+        ("zero_diagonal_index", ctypes.c_int64),
+        ("residual_inf", ctypes.c_double),
+        ("device_seconds", ctypes.c_double),
+        ("kernel_launches", ctypes.c_int64),
+    ]
+
+
+class MatrixInfo(ctypes.Structure):
+    _fields_ = [
+        ("n", ctypes.c_int64),
+        ("nnz", ctypes.c_int64),
+        ("storage", ctypes.c_int32),
+        ("device", ctypes.c_int32),
+        ("tiles", ctypes.c_int64),
+        ("max_row_nnz", ctypes.c_int64),
+        ("first_zero_diagonal", ctypes.c_int64),
+        ("device_bytes", ctypes.c_int64),
+    ]
+
+
+_lib = None
+
+
+def load():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise NativeLibraryError(
+            f"{LIB_PATH} not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
+    try:
+        L = ctypes.CDLL(LIB_PATH)
+    except OSError as err:
+        raise NativeLibraryError(f"cannot load {LIB_PATH}: {err}") from err
+    vp = ctypes.c_void_p
+    i64 = ctypes.c_int64
+    dbl = ctypes.c_double
+    L.mcr_version.restype = ctypes.c_int
+    L.mcr_version.argtypes = []
+    L.mcr_device_count.argtypes = [ctypes.POINTER(ctypes.c_int)]
+    L.mcr_matrix_create.argtypes = [i64, vp, vp, vp, ctypes.c_int, ctypes.c_int,
+                                    ctypes.POINTER(vp)]
+    L.mcr_matrix_destroy.argtypes = [vp]
+    L.mcr_matrix_destroy.restype = None
+    L.mcr_matrix_info_get.argtypes = [vp, ctypes.POINTER(MatrixInfo)]
+    L.mcr_set_stream.argtypes = [vp, vp]
+    L.mcr_set_dot_mode.argtypes = [vp, ctypes.c_int]
+    L.mcr_matvec.argtypes = [vp, vp, vp]
+    L.mcr_matvec_device.argtypes = [vp, vp, vp]
+    L.mcr_residual_inf.argtypes = [vp, vp, vp, ctypes.POINTER(dbl)]
+    for name in ("mcr_jacobi", "mcr_jacobi_device", "mcr_bicgstab", "mcr_bicgstab_device"):
+        getattr(L, name).argtypes = [vp, vp, vp, dbl, i64, vp, ctypes.POINTER(Report)]
+    L.mcr_last_error.restype = ctypes.c_char_p
+    L.mcr_last_error.argtypes = []
+    _lib = L
+    return L
+
+
+def last_error() -> str:
+    return load().mcr_last_error().decode(errors="replace")
+
+
+def device_count() -> int:
+    c = ctypes.c_int(0)
+    load().mcr_device_count(ctypes.byref(c))
+    return c.value

@@ -1,0 +1,785 @@
+// mcr.cu -- host side of libmcr.so: device storage, solve drivers and the C ABI (include/mcr.h).
+//
+// A handle uploads the reference's CSR once (sparse.py:71-98 keeps a cached scipy handle the
+// same way), derives the diagonal and the first zero-diagonal row on the device, cuts the
+// rows into shared-memory tiles, and (for >= 2/3-full matrices) re-lays the matrix out as
+// dense 32-row slabs. The Jacobi off-diagonal copy (without_diagonal, sparse.py:227-231) is
+// built on the device the first time Jacobi runs on the handle. Solves run entirely on the
+// device: every kernel reads the solver state (iteration, scalars, stop flag) from device
+// memory, so the host only enqueues batches of iterations and polls the stop flag once per
+// batch.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <cub/device/device_scan.cuh>
+
+#include "device.cuh"
+#include "mcr.h"
+
+using namespace mcr;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CK(call)                                                                        \
+    do {                                                                                \
+        cudaError_t e_ = (call);                                                        \
+        if (e_ != cudaSuccess)                                                          \
+            return fail(MCR_CUDA_ERROR, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+enum { V_B = 0, V_X, V_X1, V_R, V_Q, V_P, V_V, V_S, V_T, V_COUNT };
+
+}  // namespace
+
+struct mcr_matrix {
+    int device = 0;
+    int64_t n = 0, nnz = 0;
+    int storage = MCR_STORAGE_CSR;
+    cudaStream_t own_stream = nullptr, stream = nullptr;
+    // full matrix, CSR
+    long long* rp = nullptr;
+    int* col = nullptr;
+    double* val = nullptr;
+    int* tile_row = nullptr;
+    TileDesc* desc = nullptr;     // tiles of the full matrix
+    TileDesc* rdesc = nullptr;    // tiles of the off-diagonal copy
+    int ntiles = 0;
+    // off-diagonal copy for Jacobi (lazy)
+    long long* offlen = nullptr;
+    long long* rrp = nullptr;
+    int* rcol = nullptr;
+    double* rval = nullptr;
+    bool r_ready = false;
+    // SELL-32-sigma copies (short-row matrices): full matrix and off-diagonal R
+    struct SellDev {
+        long long* sptr = nullptr;
+        int* perm = nullptr;
+        int* col = nullptr;
+        double* val = nullptr;
+        long long* swidth = nullptr;
+        int nwin = 0;
+        long long slots = 0;
+    } sell, rsell;
+    bool use_sell = false;
+    // dense slabs
+    double* dense = nullptr;
+    int nslabs = 0;
+    // diagonal + facts
+    double* d = nullptr;
+    long long first_zero = -1;
+    long long max_row = 0;
+    // workspace
+    double* work = nullptr;
+    double* P = nullptr;
+    int nunits = 0;
+    SolveState* st = nullptr;
+    SolveState h_state{};
+    SolveState* h_st = &h_state;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    int64_t bytes = 0;
+    int seqdots = 0;
+    int spmv_grid = 1;
+    std::mutex mu;
+
+    double* vec(int k) const { return work + (size_t)k * (size_t)n; }
+    int nchunks() const { return (int)((n + CHUNK_ROWS - 1) / CHUNK_ROWS); }
+};
+
+namespace {
+
+// Device memory comes from the device's stream-ordered pool (cudaMallocAsync) with the
+// release threshold lifted, so creating and destroying handles (the end-to-end path uploads a
+// matrix per solve) recycles memory instead of paying cudaMalloc/cudaFree each time.
+template <class T>
+int dalloc(mcr_matrix* h, T** p, size_t count) {
+    *p = nullptr;
+    if (count == 0) count = 1;
+    CK(cudaMallocAsync((void**)p, sizeof(T) * count, h->stream));
+    h->bytes += (int64_t)(sizeof(T) * count);
+    return MCR_OK;
+}
+
+template <class T>
+void dfree(mcr_matrix* h, T*& p, size_t count) {
+    if (p) {
+        cudaFreeAsync(p, h->stream);
+        h->bytes -= (int64_t)(sizeof(T) * (count ? count : 1));
+        p = nullptr;
+    }
+}
+
+int keep_pool_memory(int device) {
+    static std::mutex mu;
+    static std::vector<int> done;
+    std::lock_guard<std::mutex> lk(mu);
+    if (std::find(done.begin(), done.end(), device) != done.end()) return MCR_OK;
+    cudaMemPool_t pool;
+    CK(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = UINT64_MAX;
+    CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    done.push_back(device);
+    return MCR_OK;
+}
+
+#define TRY(x)                   \
+    do {                         \
+        int rc_ = (x);           \
+        if (rc_ != MCR_OK) return rc_; \
+    } while (0)
+
+Csr csr_full(const mcr_matrix* h) {
+    return Csr{h->rp, h->col, h->val, h->desc, h->ntiles, (int)h->n};
+}
+Csr csr_off(const mcr_matrix* h) {
+    return Csr{h->rrp, h->rcol, h->rval, h->rdesc, h->ntiles, (int)h->n};
+}
+
+Vecs base_vecs(const mcr_matrix* h) {
+    Vecs V{};
+    V.b = h->vec(V_B);
+    V.d = h->d;
+    V.x = h->vec(V_X);
+    V.r = h->vec(V_R);
+    V.q = h->vec(V_Q);
+    V.p = h->vec(V_P);
+    V.v = h->vec(V_V);
+    V.s = h->vec(V_S);
+    V.t = h->vec(V_T);
+    V.P1 = h->P;
+    V.P2 = h->P + h->nunits;
+    V.x_jac0 = h->vec(V_X);
+    V.x_jac1 = h->vec(V_X1);
+    return V;
+}
+
+int ensure_work(mcr_matrix* h) {
+    if (h->work) return MCR_OK;
+    TRY(dalloc(h, &h->work, (size_t)V_COUNT * (size_t)h->n));
+    h->nunits = std::max({h->ntiles, h->nchunks(), h->nslabs, h->sell.nwin, 1});
+    TRY(dalloc(h, &h->P, (size_t)2 * h->nunits));
+    return MCR_OK;
+}
+
+// Off-diagonal copy R: row lengths from k_diag, exclusive scan (CUB), order-preserving split.
+int build_sell(mcr_matrix* h, bool offdiag, mcr_matrix::SellDev* S) {
+    const int n = (int)h->n;
+    S->nwin = (n + SELL_W - 1) / SELL_W;
+    const int nslices = S->nwin * SELL_SLICES;
+    TRY(dalloc(h, &S->perm, (size_t)S->nwin * SELL_W));
+    TRY(dalloc(h, &S->swidth, (size_t)nslices + 1));
+    TRY(dalloc(h, &S->sptr, (size_t)nslices + 1));
+    CK(cudaMemsetAsync(S->swidth + nslices, 0, sizeof(long long), h->stream));
+    k_sell_rank<<<S->nwin, SELL_W, 0, h->stream>>>(h->rp, h->offlen, n, offdiag ? 1 : 0, S->perm,
+                                                   S->swidth);
+    CK(cudaGetLastError());
+    size_t tmp = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, S->swidth, S->sptr, nslices + 1, h->stream));
+    void* dtmp = nullptr;
+    CK(cudaMallocAsync(&dtmp, tmp, h->stream));
+    CK(cub::DeviceScan::ExclusiveSum(dtmp, tmp, S->swidth, S->sptr, nslices + 1, h->stream));
+    CK(cudaFreeAsync(dtmp, h->stream));
+    CK(cudaMemcpyAsync(&S->slots, S->sptr + nslices, sizeof(long long), cudaMemcpyDeviceToHost,
+                       h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    TRY(dalloc(h, &S->col, (size_t)S->slots));
+    TRY(dalloc(h, &S->val, (size_t)S->slots));
+    const int rows = S->nwin * SELL_W;
+    k_sell_fill<<<(rows + 255) / 256, 256, 0, h->stream>>>(h->rp, h->col, h->val, S->sptr, S->perm,
+                                                           rows, offdiag ? 1 : 0, S->col, S->val);
+    CK(cudaGetLastError());
+    return MCR_OK;
+}
+
+int ensure_offdiag(mcr_matrix* h) {
+    if (h->r_ready || h->storage != MCR_STORAGE_CSR) return MCR_OK;
+    if (h->use_sell) {
+        TRY(build_sell(h, true, &h->rsell));
+        h->r_ready = true;
+        return MCR_OK;
+    }
+    const int n = (int)h->n;
+    TRY(dalloc(h, &h->rrp, (size_t)n + 1 + CSR_PAD));
+    size_t tmp = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, h->offlen, h->rrp, n + 1, h->stream));
+    void* dtmp = nullptr;
+    CK(cudaMallocAsync(&dtmp, tmp, h->stream));
+    CK(cub::DeviceScan::ExclusiveSum(dtmp, tmp, h->offlen, h->rrp, n + 1, h->stream));
+    CK(cudaFreeAsync(dtmp, h->stream));
+    long long roff = 0;
+    CK(cudaMemcpyAsync(&roff, h->rrp + n, sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    TRY(dalloc(h, &h->rcol, (size_t)roff + CSR_PAD));
+    TRY(dalloc(h, &h->rval, (size_t)roff + CSR_PAD));
+    const int threads = 256;
+    const int blocks = (int)std::min<long long>(((long long)n * 32 + threads - 1) / threads, 1 << 20);
+    if (n > 0)
+        k_split_offdiag<<<blocks, threads, 0, h->stream>>>(h->rp, h->col, h->val, n, h->rrp,
+                                                           h->rcol, h->rval);
+    CK(cudaGetLastError());
+    TRY(dalloc(h, &h->rdesc, (size_t)h->ntiles));
+    if (h->ntiles > 0)
+        k_tile_desc<<<(h->ntiles + 255) / 256, 256, 0, h->stream>>>(h->rrp, h->tile_row, h->ntiles,
+                                                                     h->rdesc);
+    CK(cudaGetLastError());
+    h->r_ready = true;
+    return MCR_OK;
+}
+
+// Greedy tiles: consecutive rows while rows <= TILE_ROWS and entries <= TILE_NNZ; a row with
+// more than TILE_NNZ entries is a tile of its own.
+std::vector<int> make_tiles(int64_t n, const int64_t* rs, long long* max_row) {
+    std::vector<int> t;
+    t.reserve((size_t)(n / 64 + 2));
+    t.push_back(0);
+    long long mr = 0;
+    int64_t r = 0;
+    while (r < n) {
+        const int64_t start = r;
+        int64_t nnz = 0;
+        while (r < n && r - start < TILE_ROWS) {
+            const int64_t len = rs[r + 1] - rs[r];
+            mr = std::max<long long>(mr, len);
+            if (nnz + len > TILE_NNZ && r > start) break;
+            nnz += len;
+            ++r;
+            if (nnz > TILE_NNZ) break;
+        }
+        t.push_back((int)r);
+    }
+    *max_row = mr;
+    return t;
+}
+
+void set_state(mcr_matrix* h, double tol, int64_t max_it) {
+    SolveState& s = *h->h_st;
+    std::memset(&s, 0, sizeof(s));
+    s.tol = tol;
+    s.max_it = max_it;
+    s.y = s.a = s.w = 1.0;
+    s.seqdots = h->seqdots;
+}
+
+int read_state(mcr_matrix* h) {
+    CK(cudaMemcpyAsync(h->h_st, h->st, sizeof(SolveState), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return MCR_OK;
+}
+
+// ---------------------------------------------------------------- kernel launchers
+template <int EPI>
+void launch_mv(mcr_matrix* h, bool offdiag, const double* x, const Vecs& V, int64_t* launches) {
+    if (h->storage == MCR_STORAGE_DENSE) {
+        k_dense<EPI><<<h->nslabs, 32, DENSE_SMEM, h->stream>>>(h->dense, (int)h->n, x, V, h->st);
+    } else if (h->use_sell) {
+        const auto& S = offdiag ? h->rsell : h->sell;
+        k_sell<EPI><<<S.nwin, SELL_W, 0, h->stream>>>(Sell{S.sptr, S.perm, S.col, S.val, S.nwin},
+                                                       x, V, h->st);
+    } else {
+        k_spmv<EPI><<<h->spmv_grid, SP_THREADS, SP_SMEM, h->stream>>>(
+            offdiag ? csr_off(h) : csr_full(h), x, V, h->st);
+    }
+    ++*launches;
+}
+
+template <int PH>
+void launch_phase(mcr_matrix* h, const Vecs& V, int64_t* launches) {
+    k_phase<PH><<<h->nchunks(), CHUNK_NT, 0, h->stream>>>(V, (int)h->n, h->st);
+    ++*launches;
+}
+
+template <int W>
+void launch_seqdot(mcr_matrix* h, const Vecs& V, int64_t* launches) {
+    if (!h->seqdots) return;
+    k_seqdot<W><<<1, SEQ_NT, 0, h->stream>>>(V, (int)h->n, h->st);
+    ++*launches;
+}
+
+int residual_into_state(mcr_matrix* h, const double* x, int64_t* launches) {
+    Vecs V = base_vecs(h);
+    launch_mv<EPI_RESID>(h, false, x, V, launches);
+    CK(cudaGetLastError());
+    return MCR_OK;
+}
+
+int prepare_inputs(mcr_matrix* h, const double* d_b, const double* d_x0, int x0_slot) {
+    const size_t bytes = sizeof(double) * (size_t)h->n;
+    CK(cudaMemcpyAsync(h->vec(V_B), d_b, bytes, cudaMemcpyDeviceToDevice, h->stream));
+    if (d_x0)
+        CK(cudaMemcpyAsync(h->vec(x0_slot), d_x0, bytes, cudaMemcpyDeviceToDevice, h->stream));
+    else
+        CK(cudaMemsetAsync(h->vec(x0_slot), 0, bytes, h->stream));
+    return MCR_OK;
+}
+
+// Batches grow 4, 8, ..., 32: a batch that overshoots the stop point only launches kernels
+// that return at their first instruction.
+int next_batch(int cur) { return std::min(cur * 2, 32); }
+
+int jacobi_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double tol, int64_t max_it,
+                double* d_x_out, mcr_report* rep) {
+    if (h->first_zero >= 0) {
+        rep->zero_diagonal_index = h->first_zero;
+        return fail(MCR_ZERO_DIAGONAL, "zero diagonal entry in row " + std::to_string(h->first_zero));
+    }
+    TRY(ensure_work(h));
+    TRY(ensure_offdiag(h));
+    TRY(prepare_inputs(h, d_b, d_x0, V_X));
+    set_state(h, tol, max_it);
+    CK(cudaMemcpyAsync(h->st, h->h_st, sizeof(SolveState), cudaMemcpyHostToDevice, h->stream));
+    Vecs V = base_vecs(h);
+    CK(cudaEventRecord(h->ev0, h->stream));
+    int64_t launched = 0, sweeps = 0;
+    int batch = 4;
+    for (;;) {
+        const int k = (int)std::min<int64_t>(batch, max_it - sweeps);
+        for (int i = 0; i < k; ++i) launch_mv<EPI_JACOBI>(h, true, nullptr, V, &launched);
+        CK(cudaGetLastError());
+        sweeps += k;
+        TRY(read_state(h));
+        if (h->h_st->stop || sweeps >= max_it) break;
+        batch = next_batch(batch);
+    }
+    const long long it = h->h_st->it;
+    const double* x = (it & 1) ? h->vec(V_X1) : h->vec(V_X);
+    TRY(residual_into_state(h, x, &launched));
+    CK(cudaEventRecord(h->ev1, h->stream));
+    TRY(read_state(h));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+    if (d_x_out)
+        CK(cudaMemcpyAsync(d_x_out, x, sizeof(double) * (size_t)h->n, cudaMemcpyDeviceToDevice,
+                           h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    const SolveState& s = *h->h_st;
+    rep->iterations = s.it;
+    rep->converged = s.stop == CONVERGED;
+    rep->residual_inf = s.resid;
+    rep->device_seconds = ms * 1e-3;
+    rep->kernel_launches = launched;
+    return s.stop == CONVERGED ? MCR_OK : MCR_NOT_CONVERGED;
+}
+
+int bicgstab_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double tol,
+                  int64_t max_it, double* d_x_out, mcr_report* rep) {
+    TRY(ensure_work(h));
+    TRY(prepare_inputs(h, d_b, d_x0, V_X));
+    set_state(h, tol, max_it);
+    CK(cudaMemcpyAsync(h->st, h->h_st, sizeof(SolveState), cudaMemcpyHostToDevice, h->stream));
+    Vecs V = base_vecs(h);
+    CK(cudaEventRecord(h->ev0, h->stream));
+    int64_t launched = 0, iters = 0;
+    launch_mv<EPI_S0>(h, false, V.x, V, &launched);  // r = b - 1.0 * M x0, q = r, p = v = 0
+    launch_seqdot<SQ_S0>(h, V, &launched);
+    CK(cudaGetLastError());
+    TRY(read_state(h));
+    int batch = 4;
+    while (!h->h_st->stop && iters < max_it) {
+        const int k = (int)std::min<int64_t>(batch, max_it - iters);
+        for (int i = 0; i < k; ++i) {
+            launch_phase<PH_A>(h, V, &launched);               // p = r + beta (p - w v)
+            launch_mv<EPI_V>(h, false, V.p, V, &launched);     // v = M p, q.v -> a
+            launch_seqdot<SQ_V>(h, V, &launched);
+            launch_phase<PH_C>(h, V, &launched);               // s = r - a v, max|s|
+            launch_mv<EPI_T>(h, false, V.s, V, &launched);     // t = M s, t.t, t.s -> w
+            launch_seqdot<SQ_T>(h, V, &launched);
+            launch_phase<PH_E>(h, V, &launched);               // x, r updates, q.r -> beta
+            launch_seqdot<SQ_E>(h, V, &launched);
+        }
+        CK(cudaGetLastError());
+        iters += k;
+        TRY(read_state(h));
+        batch = next_batch(batch);
+    }
+    TRY(residual_into_state(h, V.x, &launched));
+    CK(cudaEventRecord(h->ev1, h->stream));
+    TRY(read_state(h));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+    if (d_x_out)
+        CK(cudaMemcpyAsync(d_x_out, V.x, sizeof(double) * (size_t)h->n, cudaMemcpyDeviceToDevice,
+                           h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    const SolveState& s = *h->h_st;
+    rep->residual_inf = s.resid;
+    rep->device_seconds = ms * 1e-3;
+    rep->kernel_launches = launched;
+    rep->converged = s.stop == CONVERGED;
+    if (s.stop == BREAKDOWN) {
+        rep->iterations = s.bd_it;
+        rep->breakdown_which = s.which;
+        rep->breakdown_iteration = s.bd_it;
+        const char* names[] = {"", "y_prev*w", "q*v", "t*t"};
+        return fail(MCR_BREAKDOWN, std::string("breakdown: ") + names[s.which & 3] +
+                                       " vanished at iteration " + std::to_string(s.bd_it));
+    }
+    rep->iterations = s.it;
+    return s.stop == CONVERGED ? MCR_OK : MCR_NOT_CONVERGED;
+}
+
+void report_init(mcr_report* rep) {
+    std::memset(rep, 0, sizeof(*rep));
+    rep->zero_diagonal_index = -1;
+}
+
+// Host-pointer front end: stage b / x0 in the handle's workspace, run, copy x back.
+template <class Impl>
+int host_solve(mcr_matrix* h, const double* b, const double* x0, double tol, int64_t max_it,
+               double* x_out, mcr_report* rep, Impl impl) {
+    const size_t bytes = sizeof(double) * (size_t)h->n;
+    TRY(ensure_work(h));
+    double* db = h->vec(V_R);   // scratch slots: overwritten by the solve only after the copy
+    double* dx = h->vec(V_Q);
+    CK(cudaMemcpyAsync(db, b, bytes, cudaMemcpyHostToDevice, h->stream));
+    if (x0) CK(cudaMemcpyAsync(dx, x0, bytes, cudaMemcpyHostToDevice, h->stream));
+    double* dout = h->vec(V_V);
+    int rc = impl(h, db, x0 ? dx : nullptr, tol, max_it, dout, rep);
+    if (rc == MCR_OK || rc == MCR_NOT_CONVERGED || rc == MCR_BREAKDOWN) {
+        const double* src = dout;
+        if (rc == MCR_BREAKDOWN) src = h->vec(V_X);  // snapshot: x before that iteration
+        CK(cudaMemcpyAsync(x_out, src, bytes, cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+    }
+    return rc;
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+MCR_API int mcr_version(void) { return 100; }
+
+MCR_API const char* mcr_last_error(void) { return g_err.c_str(); }
+
+MCR_API int mcr_device_count(int* count) {
+    int c = 0;
+    cudaError_t e = cudaGetDeviceCount(&c);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        c = 0;
+    }
+    if (count) *count = c;
+    return MCR_OK;
+}
+
+MCR_API void mcr_matrix_destroy(mcr_matrix* h) {
+    if (!h) return;
+    {
+        DeviceGuard g(h->device);
+        cudaStream_t s = h->own_stream;
+        if (h->stream && h->stream != s) cudaStreamSynchronize(h->stream);
+        if (s) {
+            void* ptrs[] = {h->rp, h->col, h->val, h->tile_row, h->desc, h->rdesc, h->offlen,
+                            h->rrp, h->rcol, h->rval, h->dense, h->d, h->work, h->P, h->st,
+                            h->sell.sptr, h->sell.perm, h->sell.col, h->sell.val, h->sell.swidth,
+                            h->rsell.sptr, h->rsell.perm, h->rsell.col, h->rsell.val,
+                            h->rsell.swidth};
+            for (void* p : ptrs)
+                if (p) cudaFreeAsync(p, s);
+            cudaStreamSynchronize(s);
+        }
+        if (h->ev0) cudaEventDestroy(h->ev0);
+        if (h->ev1) cudaEventDestroy(h->ev1);
+        if (s) cudaStreamDestroy(s);
+    }
+    delete h;
+}
+
+static int set_kernel_attributes() {
+    const int sp = (int)SP_SMEM;
+    CK(cudaFuncSetAttribute(k_spmv<EPI_Y>, cudaFuncAttributeMaxDynamicSharedMemorySize, sp));
+    CK(cudaFuncSetAttribute(k_spmv<EPI_RESID>, cudaFuncAttributeMaxDynamicSharedMemorySize, sp));
+    CK(cudaFuncSetAttribute(k_spmv<EPI_JACOBI>, cudaFuncAttributeMaxDynamicSharedMemorySize, sp));
+    CK(cudaFuncSetAttribute(k_spmv<EPI_S0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sp));
+    CK(cudaFuncSetAttribute(k_spmv<EPI_V>, cudaFuncAttributeMaxDynamicSharedMemorySize, sp));
+    CK(cudaFuncSetAttribute(k_spmv<EPI_T>, cudaFuncAttributeMaxDynamicSharedMemorySize, sp));
+    return MCR_OK;
+}
+
+static int create_impl(mcr_matrix* h, int64_t n, const int64_t* rs, const int64_t* col,
+                       const double* val, int storage) {
+    TRY(keep_pool_memory(h->device));
+    CK(cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking));
+    h->stream = h->own_stream;
+    CK(cudaEventCreate(&h->ev0));
+    CK(cudaEventCreate(&h->ev1));
+    TRY(dalloc(h, &h->st, 1));
+    CK(cudaMemsetAsync(h->st, 0, sizeof(SolveState), h->stream));
+    if (n == 0) return MCR_OK;
+    const int64_t nnz = rs[n];
+    h->nnz = nnz;
+    const bool dense = storage == MCR_STORAGE_DENSE ||
+                       (storage == MCR_STORAGE_AUTO && n >= 1024 &&
+                        (double)nnz * 3.0 >= 2.0 * (double)n * (double)n);
+    h->storage = dense ? MCR_STORAGE_DENSE : MCR_STORAGE_CSR;
+
+    TRY(dalloc(h, &h->rp, (size_t)n + 1 + CSR_PAD));
+    TRY(dalloc(h, &h->col, (size_t)nnz + CSR_PAD));
+    TRY(dalloc(h, &h->val, (size_t)nnz + CSR_PAD));
+    TRY(dalloc(h, &h->d, (size_t)n));
+    TRY(dalloc(h, &h->offlen, (size_t)n + 1));
+    CK(cudaMemcpyAsync(h->rp, rs, sizeof(long long) * (size_t)(n + 1), cudaMemcpyHostToDevice,
+                       h->stream));
+    CK(cudaMemcpyAsync(h->val, val, sizeof(double) * (size_t)nnz, cudaMemcpyHostToDevice,
+                       h->stream));
+    // int64 columns -> int32 on the device, range-checked
+    {
+        long long* tmp = nullptr;
+        int* bad = nullptr;
+        CK(cudaMallocAsync((void**)&tmp, sizeof(long long) * (size_t)std::max<int64_t>(nnz, 1),
+                           h->stream));
+        CK(cudaMallocAsync((void**)&bad, sizeof(int), h->stream));
+        CK(cudaMemsetAsync(bad, 0, sizeof(int), h->stream));
+        CK(cudaMemcpyAsync(tmp, col, sizeof(long long) * (size_t)nnz, cudaMemcpyHostToDevice,
+                           h->stream));
+        if (nnz > 0)
+            k_col64to32<<<(int)std::min<int64_t>((nnz + 255) / 256, 1 << 16), 256, 0, h->stream>>>(
+                tmp, h->col, nnz, (int)n, bad);
+        CK(cudaGetLastError());
+        int hbad = 0;
+        CK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaFreeAsync(tmp, h->stream));
+        CK(cudaFreeAsync(bad, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        if (hbad) return fail(MCR_DIMENSION, "column index out of range");
+    }
+    // diagonal, first zero-diagonal row, off-diagonal row lengths
+    {
+        unsigned long long* fz = nullptr;
+        CK(cudaMallocAsync((void**)&fz, sizeof(unsigned long long), h->stream));
+        CK(cudaMemsetAsync(fz, 0xff, sizeof(unsigned long long), h->stream));
+        CK(cudaMemsetAsync(h->offlen + n, 0, sizeof(long long), h->stream));
+        k_diag<<<(int)std::min<int64_t>((n + 255) / 256, 1 << 16), 256, 0, h->stream>>>(
+            h->rp, h->col, h->val, (int)n, h->d, h->offlen, fz);
+        CK(cudaGetLastError());
+        unsigned long long hfz = 0;
+        CK(cudaMemcpyAsync(&hfz, fz, sizeof(hfz), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaFreeAsync(fz, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        h->first_zero = hfz == ~0ull ? -1 : (long long)hfz;
+    }
+    std::vector<int> tiles = make_tiles(n, rs, &h->max_row);
+    if (dense) {
+        h->nslabs = (int)((n + DSLAB - 1) / DSLAB);
+        const size_t cnt = (size_t)h->nslabs * DSLAB * (size_t)n;
+        TRY(dalloc(h, &h->dense, cnt));
+        CK(cudaMemsetAsync(h->dense, 0, sizeof(double) * cnt, h->stream));
+        k_dense_build<<<(int)n, 256, 0, h->stream>>>(h->rp, h->col, h->val, (int)n, h->dense);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(h->stream));
+        dfree(h, h->col, (size_t)nnz + CSR_PAD);
+        dfree(h, h->val, (size_t)nnz + CSR_PAD);
+        dfree(h, h->offlen, (size_t)n + 1);
+        CK(cudaFuncSetAttribute(k_dense<EPI_Y>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DENSE_SMEM));
+        CK(cudaFuncSetAttribute(k_dense<EPI_RESID>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DENSE_SMEM));
+        CK(cudaFuncSetAttribute(k_dense<EPI_JACOBI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DENSE_SMEM));
+        CK(cudaFuncSetAttribute(k_dense<EPI_S0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DENSE_SMEM));
+        CK(cudaFuncSetAttribute(k_dense<EPI_V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DENSE_SMEM));
+        CK(cudaFuncSetAttribute(k_dense<EPI_T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DENSE_SMEM));
+    } else {
+        h->ntiles = (int)tiles.size() - 1;
+        // SELL streams rows without shared-memory staging, but its epilogue operands are
+        // gathered through the row permutation; measured on C2 (profiles/) the TMA-staged
+        // tiles win (54 vs 70 us per Jacobi sweep), so SELL is opt-in.
+        h->use_sell = storage == MCR_STORAGE_SELL;
+        if (h->use_sell) TRY(build_sell(h, false, &h->sell));
+        TRY(set_kernel_attributes());
+        int sms = 0, per_sm = 0;
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv<EPI_V>, SP_THREADS, SP_SMEM));
+        h->spmv_grid = std::max(1, std::min(h->ntiles, sms * std::max(per_sm, 1)));
+        TRY(dalloc(h, &h->tile_row, tiles.size()));
+        CK(cudaMemcpyAsync(h->tile_row, tiles.data(), sizeof(int) * tiles.size(),
+                           cudaMemcpyHostToDevice, h->stream));
+        std::vector<TileDesc> desc((size_t)h->ntiles);
+        for (int t = 0; t < h->ntiles; ++t)
+            desc[(size_t)t] = TileDesc{rs[tiles[(size_t)t]], rs[tiles[(size_t)t + 1]], tiles[(size_t)t],
+                                       tiles[(size_t)t + 1]};
+        TRY(dalloc(h, &h->desc, desc.size()));
+        CK(cudaMemcpyAsync(h->desc, desc.data(), sizeof(TileDesc) * desc.size(),
+                           cudaMemcpyHostToDevice, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+    }
+    return MCR_OK;
+}
+
+MCR_API int mcr_matrix_create(int64_t n, const int64_t* rstart, const int64_t* col,
+                              const double* nonzero, int device, int storage, mcr_matrix** out) {
+    if (!out) return fail(MCR_INVALID_ARGUMENT, "out is NULL");
+    *out = nullptr;
+    if (n < 0 || n >= INT_MAX) return fail(MCR_DIMENSION, "dimension out of range");
+    if (n > 0 && (!rstart || (rstart[n] > 0 && (!col || !nonzero))))
+        return fail(MCR_INVALID_ARGUMENT, "NULL CSR array");
+    if (n > 0) {
+        if (rstart[0] != 0) return fail(MCR_DIMENSION, "malformed rstart vector");
+        for (int64_t i = 0; i < n; ++i)
+            if (rstart[i + 1] < rstart[i]) return fail(MCR_DIMENSION, "rstart must be nondecreasing");
+    }
+    int ndev = 0;
+    mcr_device_count(&ndev);
+    if (device < 0 || device >= ndev)
+        return fail(MCR_CUDA_ERROR, "no CUDA device " + std::to_string(device) + " (" +
+                                        std::to_string(ndev) + " visible)");
+    DeviceGuard g(device);
+    mcr_matrix* h = new mcr_matrix();
+    h->device = device;
+    h->n = n;
+    int rc = create_impl(h, n, rstart, col, nonzero, storage);
+    if (rc != MCR_OK) {
+        std::string msg = g_err;
+        mcr_matrix_destroy(h);
+        g_err = msg;
+        return rc;
+    }
+    *out = h;
+    return MCR_OK;
+}
+
+MCR_API int mcr_matrix_info_get(const mcr_matrix* h, mcr_matrix_info* info) {
+    if (!h || !info) return fail(MCR_INVALID_ARGUMENT, "NULL argument");
+    info->n = h->n;
+    info->nnz = h->nnz;
+    info->storage = h->storage == MCR_STORAGE_DENSE ? MCR_STORAGE_DENSE
+                    : (h->use_sell ? MCR_STORAGE_SELL : MCR_STORAGE_TILES);
+    info->device = h->device;
+    info->tiles = h->ntiles;
+    info->max_row_nnz = h->max_row;
+    info->first_zero_diagonal = h->first_zero;
+    info->device_bytes = h->bytes;
+    return MCR_OK;
+}
+
+MCR_API int mcr_set_dot_mode(mcr_matrix* h, int mode) {
+    if (!h) return fail(MCR_INVALID_ARGUMENT, "NULL handle");
+    if (mode != MCR_DOTS_TREE && mode != MCR_DOTS_SEQUENTIAL)
+        return fail(MCR_INVALID_ARGUMENT, "unknown dot mode");
+    std::lock_guard<std::mutex> lk(h->mu);
+    h->seqdots = mode == MCR_DOTS_SEQUENTIAL;
+    return MCR_OK;
+}
+
+MCR_API int mcr_set_stream(mcr_matrix* h, void* stream) {
+    if (!h) return fail(MCR_INVALID_ARGUMENT, "NULL handle");
+    std::lock_guard<std::mutex> lk(h->mu);
+    h->stream = stream ? (cudaStream_t)stream : h->own_stream;
+    return MCR_OK;
+}
+
+MCR_API int mcr_matvec_device(mcr_matrix* h, const double* d_x, double* d_y) {
+    if (!h) return fail(MCR_INVALID_ARGUMENT, "NULL handle");
+    std::lock_guard<std::mutex> lk(h->mu);
+    if (h->n == 0) return MCR_OK;
+    DeviceGuard g(h->device);
+    Vecs V{};
+    V.y = d_y;
+    int64_t launched = 0;
+    launch_mv<EPI_Y>(h, false, d_x, V, &launched);
+    CK(cudaGetLastError());
+    return MCR_OK;
+}
+
+MCR_API int mcr_matvec(mcr_matrix* h, const double* x, double* y) {
+    if (!h) return fail(MCR_INVALID_ARGUMENT, "NULL handle");
+    std::lock_guard<std::mutex> lk(h->mu);
+    if (h->n == 0) return MCR_OK;
+    DeviceGuard g(h->device);
+    TRY(ensure_work(h));
+    const size_t bytes = sizeof(double) * (size_t)h->n;
+    CK(cudaMemcpyAsync(h->vec(V_P), x, bytes, cudaMemcpyHostToDevice, h->stream));
+    Vecs V{};
+    V.y = h->vec(V_V);
+    int64_t launched = 0;
+    launch_mv<EPI_Y>(h, false, h->vec(V_P), V, &launched);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(y, h->vec(V_V), bytes, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return MCR_OK;
+}
+
+MCR_API int mcr_residual_inf(mcr_matrix* h, const double* x, const double* b, double* out) {
+    if (!h || !out) return fail(MCR_INVALID_ARGUMENT, "NULL argument");
+    std::lock_guard<std::mutex> lk(h->mu);
+    *out = 0.0;
+    if (h->n == 0) return MCR_OK;
+    DeviceGuard g(h->device);
+    TRY(ensure_work(h));
+    const size_t bytes = sizeof(double) * (size_t)h->n;
+    CK(cudaMemcpyAsync(h->vec(V_P), x, bytes, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaMemcpyAsync(h->vec(V_B), b, bytes, cudaMemcpyHostToDevice, h->stream));
+    set_state(h, 0.0, 0);
+    CK(cudaMemcpyAsync(h->st, h->h_st, sizeof(SolveState), cudaMemcpyHostToDevice, h->stream));
+    int64_t launched = 0;
+    TRY(residual_into_state(h, h->vec(V_P), &launched));
+    TRY(read_state(h));
+    *out = h->h_st->resid;
+    return MCR_OK;
+}
+
+#define SOLVE_PROLOGUE                                                          \
+    if (!h || !rep) return fail(MCR_INVALID_ARGUMENT, "NULL argument");        \
+    if (!(tol > 0.0)) return fail(MCR_INVALID_ARGUMENT, "tolerance must be positive"); \
+    if (max_it < 1) return fail(MCR_INVALID_ARGUMENT, "max_iterations must be at least 1"); \
+    std::lock_guard<std::mutex> lk(h->mu);                                      \
+    report_init(rep);                                                           \
+    if (h->n == 0) {                                                            \
+        rep->converged = 1;                                                     \
+        return MCR_OK;                                                          \
+    }                                                                           \
+    DeviceGuard g(h->device);
+
+MCR_API int mcr_jacobi_device(mcr_matrix* h, const double* d_b, const double* d_x0, double tol,
+                              int64_t max_it, double* d_x_out, mcr_report* rep) {
+    SOLVE_PROLOGUE
+    return jacobi_impl(h, d_b, d_x0, tol, max_it, d_x_out, rep);
+}
+
+MCR_API int mcr_bicgstab_device(mcr_matrix* h, const double* d_b, const double* d_x0, double tol,
+                                int64_t max_it, double* d_x_out, mcr_report* rep) {
+    SOLVE_PROLOGUE
+    return bicgstab_impl(h, d_b, d_x0, tol, max_it, d_x_out, rep);
+}
+
+MCR_API int mcr_jacobi(mcr_matrix* h, const double* b, const double* x0, double tol,
+                       int64_t max_it, double* x_out, mcr_report* rep) {
+    SOLVE_PROLOGUE
+    if (h->first_zero >= 0) {
+        rep->zero_diagonal_index = h->first_zero;
+        return fail(MCR_ZERO_DIAGONAL, "zero diagonal entry in row " + std::to_string(h->first_zero));
+    }
+    return host_solve(h, b, x0, tol, max_it, x_out, rep, jacobi_impl);
+}
+
+MCR_API int mcr_bicgstab(mcr_matrix* h, const double* b, const double* x0, double tol,
+                         int64_t max_it, double* x_out, mcr_report* rep) {
+    SOLVE_PROLOGUE
+    return host_solve(h, b, x0, tol, max_it, x_out, rep, bicgstab_impl);
+}
+
+}  // extern "C"

@@ -1,0 +1,315 @@
+"""Drop-in GPU solvers with the reference's interface (mcreach/solvers.py).
+
+Every public name here mirrors ``/root/reference/pkg/src/mcreach/solvers.py``:
+
+* ``SolverConfig`` (:81-109), ``SolveResult`` (:112-120), ``SolverError`` / ``ZeroDiagonal`` /
+  ``NotConverged`` / ``Breakdown`` (:43-78) -- same fields, validation and messages;
+* ``jacobi_solve`` (:194-230) and ``bicgstab_solve`` (:399-426) -- same signature
+  ``fn(m, b, config=None) -> SolveResult``, same stopping rules, same exceptions, same
+  ``wall_time`` region (after the right-hand-side check, through the final residual);
+* ``residual_inf_norm`` (:123-133) and ``matvec`` (sparse.py:184-191);
+* ``SOLVERS`` (:494-499) with the GPU methods ``jacobi-gpu`` and ``bicgstab-gpu``.
+
+The arithmetic runs in libmcr.so (CUDA, sm_100a) behind the C ABI in include/mcr.h; the
+matrix is uploaded once per ``CsrMatrix`` object and cached while that object lives, like
+the reference caches its scipy handle (sparse.py:91-98). ``plugin.install()`` registers these
+methods into the reference's own ``mcreach.solvers.SOLVERS``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+import time
+import weakref
+from dataclasses import dataclass
+from typing import Callable, Optional
+
+import numpy as np
+
+from . import _lib
+from .sparse import DimensionMismatch
+
+__all__ = [
+    "SolverConfig", "SolveResult", "SolverError", "ZeroDiagonal", "NotConverged", "Breakdown",
+    "DeviceMatrix", "device_matrix", "jacobi_solve", "bicgstab_solve", "bicgstab_solve_exact",
+    "residual_inf_norm",
+    "matvec", "SOLVERS",
+]
+
+
+class SolverError(RuntimeError):
+    """Base class for solver failures (solvers.py:43-44)."""
+
+
+class ZeroDiagonal(SolverError):
+    def __init__(self, index: int):
+        super().__init__(f"zero diagonal entry in row {index}")
+        self.index = index
+
+
+class NotConverged(SolverError):
+    def __init__(self, result: "SolveResult"):
+        super().__init__(
+            f"no convergence after {result.iterations} iterations "
+            f"(residual sup-norm {result.residual_inf:.3e})")
+        self.result = result
+        self.iterations = result.iterations
+        self.residual_inf = result.residual_inf
+
+
+class Breakdown(SolverError):
+    def __init__(self, which: str, iteration: int, result: "SolveResult"):
+        super().__init__(f"breakdown: {which} vanished at iteration {iteration}")
+        self.which = which
+        self.iteration = iteration
+        self.result = result
+
+
+@dataclass(frozen=True)
+class SolverConfig:
+    """solvers.py:81-109, plus two GPU fields.
+
+    ``device``: CUDA ordinal of the solve. ``dot_products``: ``"tree"`` (default) reduces
+    BiCGStab's inner products with deterministic fixed-shape trees fused into the producing
+    kernels; ``"sequential"`` reproduces the reference's strictly left-to-right
+    ``_dot_ascending`` (solvers.py:136-141) bit for bit, at one dependent add per element.
+    """
+
+    tolerance: float = 1e-10
+    max_iterations: int = 10_000
+    guess_seed: Optional[int] = None
+    workers: Optional[int] = None
+    parallel_dot_products: bool = False
+    device: int = 0
+    dot_products: str = "tree"
+
+    def __post_init__(self):
+        if not self.tolerance > 0.0:
+            raise ValueError("tolerance must be positive")
+        if self.max_iterations < 1:
+            raise ValueError("max_iterations must be at least 1")
+        if self.workers is not None and self.workers < 1:
+            raise ValueError("workers must be at least 1")
+        if self.dot_products not in ("tree", "sequential"):
+            raise ValueError("dot_products must be 'tree' or 'sequential'")
+
+    def resolved_workers(self) -> int:
+        return self.workers if self.workers is not None else (os.cpu_count() or 1)
+
+
+@dataclass(frozen=True, eq=False)
+class SolveResult:
+    x: np.ndarray
+    iterations: int
+    converged: bool
+    residual_inf: float
+    wall_time: float
+
+
+# ----------------------------------------------------------------------------- device handle
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+class DeviceMatrix:
+    """Device-resident copy of a CSR matrix (one libmcr handle)."""
+
+    def __init__(self, m, device: int = 0, storage: int = _lib.STORAGE_AUTO):
+        L = _lib.load()
+        n = int(m.n)
+        rs = np.ascontiguousarray(m.rstart, dtype=np.int64)
+        col = np.ascontiguousarray(m.col, dtype=np.int64)
+        val = np.ascontiguousarray(m.nonzero, dtype=np.float64)
+        h = ctypes.c_void_p()
+        rc = L.mcr_matrix_create(n, _ptr(rs), _ptr(col), _ptr(val), int(device), int(storage),
+                                 ctypes.byref(h))
+        if rc != _lib.MCR_OK:
+            _raise_native(rc)
+        self._h = h
+        self._L = L
+        self.n = n
+        self.device = int(device)
+        self.lock = threading.Lock()
+        self._finalizer = weakref.finalize(self, L.mcr_matrix_destroy, h)
+
+    @property
+    def handle(self) -> ctypes.c_void_p:
+        return self._h
+
+    def info(self) -> dict:
+        inf = _lib.MatrixInfo()
+        self._L.mcr_matrix_info_get(self._h, ctypes.byref(inf))
+        return {f: getattr(inf, f) for f, _ in _lib.MatrixInfo._fields_}
+
+    def close(self) -> None:
+        self._finalizer()
+
+    def matvec(self, x) -> np.ndarray:
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.empty(self.n)
+        rc = self._L.mcr_matvec(self._h, _ptr(x), _ptr(y))
+        if rc != _lib.MCR_OK:
+            _raise_native(rc)
+        return y
+
+    def residual_inf(self, x, b) -> float:
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        out = ctypes.c_double(0.0)
+        rc = self._L.mcr_residual_inf(self._h, _ptr(x), _ptr(b), ctypes.byref(out))
+        if rc != _lib.MCR_OK:
+            _raise_native(rc)
+        return out.value
+
+    def solve(self, method: str, b: np.ndarray, x0: Optional[np.ndarray], tol: float,
+              max_it: int, dots: str = "tree"):
+        fn = {"jacobi": self._L.mcr_jacobi, "bicgstab": self._L.mcr_bicgstab}[method]
+        mode = _lib.DOTS_SEQUENTIAL if dots == "sequential" else _lib.DOTS_TREE
+        rc = self._L.mcr_set_dot_mode(self._h, mode)
+        if rc != _lib.MCR_OK:
+            _raise_native(rc)
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        x = np.empty(self.n)
+        x0p = None
+        if x0 is not None:
+            x0 = np.ascontiguousarray(x0, dtype=np.float64)
+            x0p = _ptr(x0)
+        rep = _lib.Report()
+        rc = fn(self._h, _ptr(b), x0p, float(tol), int(max_it), _ptr(x), ctypes.byref(rep))
+        return rc, x, rep
+
+
+_cache: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+_cache_lock = threading.Lock()
+
+
+def device_matrix(m, device: int = 0) -> DeviceMatrix:
+    """Cached device copy of ``m`` (uploaded once per matrix object and device)."""
+    with _cache_lock:
+        per = _cache.get(m)
+        if per is None:
+            per = {}
+            try:
+                _cache[m] = per
+            except TypeError:  # not weak-referenceable: no caching
+                return DeviceMatrix(m, device)
+        dm = per.get(device)
+        if dm is None:
+            dm = DeviceMatrix(m, device)
+            per[device] = dm
+        return dm
+
+
+def _raise_native(rc: int):
+    msg = _lib.last_error()
+    if rc == _lib.MCR_DIMENSION:
+        raise DimensionMismatch(msg)
+    if rc == _lib.MCR_INVALID_ARGUMENT:
+        raise ValueError(msg)
+    raise _lib.NativeLibraryError(f"libmcr error {rc}: {msg}")
+
+
+# ----------------------------------------------------------------------------- solvers
+
+def _check_system(m, b) -> np.ndarray:
+    """solvers.py:144-150"""
+    b = np.asarray(b, dtype=np.float64)
+    if b.shape != (m.n,):
+        raise DimensionMismatch(f"right-hand side of shape {b.shape} against dimension {m.n}")
+    return b
+
+
+def _initial_guess(n: int, cfg) -> Optional[np.ndarray]:
+    """solvers.py:153-156; None means the zero vector (filled on the device)."""
+    seed = getattr(cfg, "guess_seed", None)
+    if seed is None:
+        return None
+    return np.random.default_rng(seed).random(n)
+
+
+def _empty_result(start: float) -> SolveResult:
+    return SolveResult(np.zeros(0), 0, True, 0.0, time.perf_counter() - start)
+
+
+def _solve(method: str, m, b, config, dots: Optional[str] = None) -> SolveResult:
+    cfg = config or SolverConfig()
+    b = _check_system(m, b)
+    start = time.perf_counter()
+    if m.n == 0:
+        return _empty_result(start)
+    dm = device_matrix(m, int(getattr(cfg, "device", 0) or 0))
+    x0 = _initial_guess(m.n, cfg)
+    with dm.lock:
+        rc, x, rep = dm.solve(method, b, x0, cfg.tolerance, cfg.max_iterations,
+                              dots or getattr(cfg, "dot_products", "tree"))
+    if rc == _lib.MCR_ZERO_DIAGONAL:
+        raise ZeroDiagonal(int(rep.zero_diagonal_index))
+    if rc not in (_lib.MCR_OK, _lib.MCR_NOT_CONVERGED, _lib.MCR_BREAKDOWN):
+        _raise_native(rc)
+    iterations = int(rep.iterations)
+    result = SolveResult(x, iterations, rc == _lib.MCR_OK, float(rep.residual_inf),
+                         time.perf_counter() - start)
+    if rc == _lib.MCR_BREAKDOWN:
+        raise Breakdown(_lib.BREAKDOWN_NAMES[int(rep.breakdown_which)],
+                        int(rep.breakdown_iteration), result)
+    if rc == _lib.MCR_NOT_CONVERGED:
+        raise NotConverged(result)
+    return result
+
+
+def jacobi_solve(m, b, config: Optional[SolverConfig] = None) -> SolveResult:
+    """Jacobi iteration on the GPU (solvers.py:194-230 semantics, bit-identical iterates).
+
+    Raises ZeroDiagonal before any sweep, NotConverged after ``max_iterations`` sweeps with
+    the last iterate attached.
+    """
+    return _solve("jacobi", m, b, config)
+
+
+def bicgstab_solve(m, b, config: Optional[SolverConfig] = None) -> SolveResult:
+    """Un-preconditioned BiCGStab on the GPU (solvers.py:399-491 semantics).
+
+    Raises Breakdown (snapshot before the failing iteration) or NotConverged.
+    """
+    return _solve("bicgstab", m, b, config)
+
+
+def bicgstab_solve_exact(m, b, config: Optional[SolverConfig] = None) -> SolveResult:
+    """BiCGStab with the reference's sequential inner products: bit-identical to
+    ``mcreach.bicgstab_solve`` (x, iteration count, residual, breakdowns)."""
+    return _solve("bicgstab", m, b, config, dots="sequential")
+
+
+def residual_inf_norm(m, x, b) -> float:
+    """solvers.py:123-133 on the device."""
+    x = np.asarray(x, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    if x.shape != (m.n,) or b.shape != (m.n,):
+        raise DimensionMismatch(f"system of dimension {m.n} with x{x.shape}, b{b.shape}")
+    if m.n == 0:
+        return 0.0
+    dm = device_matrix(m)
+    with dm.lock:
+        return dm.residual_inf(x, b)
+
+
+def matvec(m, x) -> np.ndarray:
+    """sparse.py:184-191 on the device (bit-identical row sums)."""
+    x = np.asarray(x, dtype=np.float64)
+    if x.shape != (m.n,):
+        raise DimensionMismatch(f"vector of shape {x.shape} against dimension {m.n}")
+    if m.n == 0:
+        return np.zeros(0)
+    dm = device_matrix(m)
+    with dm.lock:
+        return dm.matvec(x)
+
+
+SOLVERS: dict[str, Callable[..., SolveResult]] = {
+    "jacobi-gpu": jacobi_solve,
+    "bicgstab-gpu": bicgstab_solve,
+    "bicgstab-gpu-exact": bicgstab_solve_exact,
+}

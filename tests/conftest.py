@@ -13,3 +13,9 @@ if HERE not in sys.path:
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (runs the CUDA path through the C-ABI)")
     config.addinivalue_line("markers", "slow: larger systems (C2 scale)")
+
+# the reference package travels to the GPU box under baseline/_ref (git-ignored); tests that
+# exercise the plugin registration import it from there when present
+_REF = os.path.join(ROOT, "baseline", "_ref")
+if os.path.isdir(os.path.join(_REF, "mcreach")) and _REF not in sys.path:
+    sys.path.append(_REF)
