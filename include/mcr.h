@@ -52,14 +52,17 @@ enum { MCR_BD_NONE = 0, MCR_BD_Y_PREV_W = 1, MCR_BD_Q_V = 2, MCR_BD_T_T = 3 };
 /* Device storage selection for mcr_matrix_create. AUTO picks dense 32-row slabs when the
  * matrix is at least 2/3 full and n >= 1024; otherwise CSR, laid out as SELL-32-sigma when the
  * caller asks for it (coalesced thread-per-row streaming) and as CSR tiles staged by
- * TMA bulk copies otherwise (the default). SELL / TILES force one CSR layout. mcr_matrix_info reports the
+ * TMA bulk copies otherwise (the default). SELL / TILES force one CSR layout. Tiled systems
+ * whose tiles all fit on the GPU at once (<= 2 tiles per SM) solve in ONE cooperative launch
+ * (grid barriers between sweeps); TILES_STREAM opts out of that. mcr_matrix_info reports the
  * layout in use (DENSE, SELL or TILES). */
 enum {
     MCR_STORAGE_AUTO = 0,
     MCR_STORAGE_CSR = 1,
     MCR_STORAGE_DENSE = 2,
     MCR_STORAGE_SELL = 3,
-    MCR_STORAGE_TILES = 4
+    MCR_STORAGE_TILES = 4,
+    MCR_STORAGE_TILES_STREAM = 5 /* tiles, but never the single-launch small-system solvers */
 };
 
 typedef struct mcr_matrix mcr_matrix;

@@ -18,6 +18,7 @@
 //          its row's strictly sequential sum.
 #pragma once
 
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -168,6 +169,14 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// Programmatic dependent launch: solve kernels are launched with the PDL attribute, so the
+// next kernel's CTAs can be scheduled while this grid drains; griddep_wait() blocks until the
+// previous grid has completed and its writes are visible, griddep_launch() lets the next one
+// start launching. Both are no-ops for a kernel launched without the attribute.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 // Named barrier among the first `count` threads (count multiple of 32).
 __device__ __forceinline__ void named_sync(int id, int count) {
@@ -451,6 +460,8 @@ __global__ void __launch_bounds__(SP_THREADS, MCR_SP_MINB) k_spmv(Csr A, const d
     __shared__ double s_red[SP_THREADS / 32];
     __shared__ unsigned long long s_redu[SP_THREADS / 32];
     __shared__ int s_flag;
+    griddep_wait();
+    griddep_launch();
     if constexpr (epi_checks_stop<EPI>()) {
         if (st->stop) return;
     }
@@ -605,6 +616,10 @@ constexpr int SELL_C = 32;
 constexpr int SELL_W = 256;              // rows per window = threads per CTA
 constexpr int SELL_SLICES = SELL_W / SELL_C;
 constexpr int SELL_UNROLL = 8;           // entries in flight per lane
+#ifndef MCR_SELL_CTA
+#define MCR_SELL_CTA 256
+#endif
+constexpr int SELL_CTA = MCR_SELL_CTA;   // threads per SpMV CTA: slices of similar width
 constexpr int SELL_MAX_MEAN = 32;
 
 struct Sell {
@@ -616,17 +631,19 @@ struct Sell {
 };
 
 template <int EPI>
-__global__ void __launch_bounds__(SELL_W) k_sell(Sell A, const double* __restrict__ x, Vecs V,
-                                                 SolveState* st) {
-    __shared__ double s_red[SELL_W / 32];
-    __shared__ unsigned long long s_redu[SELL_W / 32];
+__global__ void __launch_bounds__(SELL_CTA) k_sell(Sell A, const double* __restrict__ x, Vecs V,
+                                                   SolveState* st) {
+    __shared__ double s_red[SELL_CTA / 32];
+    __shared__ unsigned long long s_redu[SELL_CTA / 32];
     __shared__ int s_flag;
+    griddep_wait();
+    griddep_launch();
     if constexpr (epi_checks_stop<EPI>()) {
         if (st->stop) return;
     }
     const double* xin = jacobi_select<EPI>(x, V, st);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int slice = blockIdx.x * SELL_SLICES + warp;
+    const int slice = blockIdx.x * (SELL_CTA / 32) + warp;
     const long long b0 = __ldg(A.sptr + slice);
     const int width = (int)((__ldg(A.sptr + slice + 1) - b0) / SELL_C);
     const int row = __ldg(A.perm + slice * SELL_C + lane);
@@ -654,14 +671,14 @@ __global__ void __launch_bounds__(SELL_W) k_sell(Sell A, const double* __restric
     unsigned long long mb = 0;
     if (row >= 0) epi_store<EPI>(V, row, acc, in, p1, p2, mb);
     if constexpr (epi_has_dot<EPI>()) {
-        p1 = group_sum<SELL_W / 32, 0>(p1, s_red);
+        p1 = group_sum<SELL_CTA / 32, 0>(p1, s_red);
         if (threadIdx.x == 0) V.P1[blockIdx.x] = p1;
         if constexpr (EPI == EPI_T) {
-            p2 = group_sum<SELL_W / 32, 0>(p2, s_red);
+            p2 = group_sum<SELL_CTA / 32, 0>(p2, s_red);
             if (threadIdx.x == 0) V.P2[blockIdx.x] = p2;
         }
     }
-    kernel_finish<SELL_W, EPI>(V, st, gridDim.x, mb, s_red, s_redu, &s_flag);
+    kernel_finish<SELL_CTA, EPI>(V, st, gridDim.x, mb, s_red, s_redu, &s_flag);
 }
 
 // SELL build 1/2: per window, order rows by (length desc, index asc); record each slice's
@@ -685,8 +702,9 @@ __global__ void __launch_bounds__(SELL_W) k_sell_rank(const long long* __restric
     lens[rank] = len;  // lengths in slot order
     __syncthreads();
     if (threadIdx.x < SELL_SLICES) {
-        const int l = lens[threadIdx.x * SELL_C];
-        swidth[blockIdx.x * SELL_SLICES + threadIdx.x] = (long long)(l > 0 ? l : 0) * SELL_C;
+        int l = 0;
+        for (int k = 0; k < SELL_C; ++k) l = max(l, lens[threadIdx.x * SELL_C + k]);
+        swidth[blockIdx.x * SELL_SLICES + threadIdx.x] = (long long)l * SELL_C;
     }
 }
 
@@ -719,6 +737,246 @@ __global__ void k_sell_fill(const long long* __restrict__ rp, const int* __restr
     }
 }
 
+// ---------------------------------------------------------------- persistent small-system solvers
+// For systems whose tiles all fit on the GPU at once (ntiles <= co-resident CTAs, e.g. C1 and
+// the Table-1 shapes) one cooperative kernel runs the whole solve: sweeps / iterations are
+// separated by grid barriers instead of kernel launches, and every CTA reduces the per-tile
+// partials itself in the same fixed order, so all CTAs hold bit-identical scalars without a
+// round trip through global state.
+namespace cg = cooperative_groups;
+constexpr int SM_NT = TILE_ROWS;
+
+struct SmallSmem {
+    double prod[TILE_NNZ];
+    int rp[TILE_ROWS + 1];
+    double red[SM_NT / 32];
+    unsigned long long redu[SM_NT / 32];
+};
+
+// Row sums of one tile straight from HBM/L2: coalesced val/col loads, products staged in
+// shared memory, then thread r adds its row left to right (long rows streamed in chunks).
+__device__ __forceinline__ double tile_rowsum_direct(const Csr& A, int t, const double* __restrict__ x,
+                                                     SmallSmem& sm, int& row) {
+    const int tid = threadIdx.x;
+    const TileDesc d = A.desc[t];
+    const int nrows = d.r1 - d.r0;
+    const long long len = d.e1 - d.e0;
+    row = tid < nrows ? d.r0 + tid : -1;
+    double acc = 0.0;
+    if (len <= TILE_NNZ) {
+        for (int k = tid; k <= nrows; k += SM_NT) sm.rp[k] = (int)(A.rp[d.r0 + k] - d.e0);
+        for (int k = tid; k < len; k += SM_NT)
+            sm.prod[k] = dmul(A.val[d.e0 + k], __ldg(x + A.col[d.e0 + k]));
+        __syncthreads();
+        if (tid < nrows) {
+            const int b = sm.rp[tid], e = sm.rp[tid + 1];
+            for (int k = b; k < e; ++k) acc = dadd(acc, sm.prod[k]);
+        }
+        __syncthreads();
+    } else {
+        double a = 0.0;
+        for (long long b0 = d.e0; b0 < d.e1; b0 += TILE_NNZ) {
+            const int clen = (int)((d.e1 - b0) < TILE_NNZ ? (d.e1 - b0) : TILE_NNZ);
+            for (int k = tid; k < clen; k += SM_NT)
+                sm.prod[k] = dmul(A.val[b0 + k], __ldg(x + A.col[b0 + k]));
+            __syncthreads();
+            if (tid == 0)
+                for (int k = 0; k < clen; ++k) a = dadd(a, sm.prod[k]);
+            __syncthreads();
+        }
+        acc = a;
+    }
+    return acc;
+}
+
+// Same fixed-order reduction as reduce_partials, run by every CTA (L2 reads: the partials
+// were just written by other CTAs).
+__device__ __forceinline__ double all_reduce_partials(const double* P, int count, double* red) {
+    double acc = 0.0;
+    for (int k = threadIdx.x; k < count; k += SM_NT) acc = dadd(acc, __ldcg(P + k));
+    acc = group_sum<SM_NT / 32, 0>(acc, red);
+    if (threadIdx.x == 0) red[0] = acc;
+    __syncthreads();
+    acc = red[0];
+    __syncthreads();
+    return acc;
+}
+
+__device__ __forceinline__ double read_max(unsigned long long* slot) {
+    return bits2d(__ldcg(slot));
+}
+
+// Jacobi, all sweeps in one launch. maxslot[3] are zero on entry.
+__global__ void __launch_bounds__(SM_NT) k_jacobi_small(Csr R, Vecs V, SolveState* st,
+                                                        unsigned long long* maxslot) {
+    __shared__ SmallSmem sm;
+    cg::grid_group grid = cg::this_grid();
+    const double tol = st->tol;
+    const long long max_it = st->max_it;
+    long long it = 0;
+    int stop = RUNNING;
+    while (stop == RUNNING) {
+        ++it;
+        const double* xin = (it & 1) ? V.x_jac0 : V.x_jac1;
+        double* xout = (it & 1) ? V.x_jac1 : V.x_jac0;
+        unsigned long long mb = 0;
+        for (int t = blockIdx.x; t < R.ntiles; t += gridDim.x) {
+            int row;
+            const double s = tile_rowsum_direct(R, t, xin, sm, row);
+            if (row >= 0) {
+                const double xn = ddiv(dsub(V.b[row], s), V.d[row]);   // (b - R x) / d
+                xout[row] = xn;
+                mb = umax(mb, absbits(dsub(xn, xin[row])));
+            }
+        }
+        mb = group_max<SM_NT / 32, 0>(mb, sm.redu);
+        if (threadIdx.x == 0 && mb) atomicMax(&maxslot[it % 3], mb);
+        // slot (it+1)%3 was last read before the previous barrier by every CTA: clear it for
+        // the next sweep before this barrier, so no CTA can add to it before it is cleared
+        if (blockIdx.x == 0 && threadIdx.x == 0) maxslot[(it + 1) % 3] = 0ull;
+        grid.sync();
+        const double md = read_max(&maxslot[it % 3]);
+        if (md <= tol) stop = CONVERGED;
+        else if (it >= max_it) stop = NOTCONV;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        st->it = it;
+        st->stop = stop;
+    }
+}
+
+// BiCGStab, whole solve in one launch (solvers.py:450-491). maxslot[2] zero on entry;
+// P1/P2 hold ntiles partials.
+__global__ void __launch_bounds__(SM_NT) k_bicg_small(Csr A, Vecs V, SolveState* st,
+                                                      unsigned long long* maxslot) {
+    __shared__ SmallSmem sm;
+    cg::grid_group grid = cg::this_grid();
+    const double tol = st->tol;
+    const long long max_it = st->max_it;
+    const int nt = A.ntiles;
+    // setup: r = b - 1.0 * M x0, q = r, p = v = 0
+    unsigned long long mb = 0;
+    for (int t = blockIdx.x; t < nt; t += gridDim.x) {
+        int row;
+        const double s = tile_rowsum_direct(A, t, V.x, sm, row);
+        double p1 = 0.0;
+        if (row >= 0) {
+            const double r = dsub(V.b[row], dmul(1.0, s));
+            V.r[row] = r; V.q[row] = r; V.p[row] = 0.0; V.v[row] = 0.0;
+            mb = umax(mb, absbits(r));
+            p1 = dmul(r, r);
+        }
+        p1 = group_sum<SM_NT / 32, 0>(p1, sm.red);
+        if (threadIdx.x == 0) V.P1[t] = p1;
+    }
+    mb = group_max<SM_NT / 32, 0>(mb, sm.redu);
+    if (threadIdx.x == 0 && mb) atomicMax(&maxslot[0], mb);
+    grid.sync();
+    int stop = RUNNING, which = 0;
+    long long it = 0, bd_it = 0;
+    double y = 1.0, a = 1.0, w = 1.0, beta = 0.0;
+    {
+        const double mr = read_max(&maxslot[0]);
+        const double qr = all_reduce_partials(V.P1, nt, sm.red);
+        if (mr <= tol) {
+            stop = CONVERGED;
+        } else {
+            const double denom = dmul(y, w);
+            y = qr;
+            if (tiny(denom)) { stop = BREAKDOWN; which = 1; bd_it = 1; }
+            else beta = ddiv(dmul(qr, a), denom);
+        }
+    }
+    while (stop == RUNNING) {
+        const long long cur = it + 1;
+        // A: p = r + beta (p - w v)
+        for (int t = blockIdx.x; t < nt; t += gridDim.x) {
+            const TileDesc d = A.desc[t];
+            const int row = d.r0 + (int)threadIdx.x;
+            if (row < d.r1) V.p[row] = dadd(V.r[row], dmul(beta, dsub(V.p[row], dmul(w, V.v[row]))));
+        }
+        grid.sync();
+        // B: v = M p, q.v
+        for (int t = blockIdx.x; t < nt; t += gridDim.x) {
+            int row;
+            const double s = tile_rowsum_direct(A, t, V.p, sm, row);
+            double p1 = 0.0;
+            if (row >= 0) { V.v[row] = s; p1 = dmul(V.q[row], s); }
+            p1 = group_sum<SM_NT / 32, 0>(p1, sm.red);
+            if (threadIdx.x == 0) V.P1[t] = p1;
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0) maxslot[1] = 0ull;
+        grid.sync();
+        const double qv = all_reduce_partials(V.P1, nt, sm.red);
+        if (tiny(qv)) { stop = BREAKDOWN; which = 2; bd_it = cur; break; }
+        a = ddiv(y, qv);
+        // C: s = r - a v, max|s|
+        mb = 0;
+        for (int t = blockIdx.x; t < nt; t += gridDim.x) {
+            const TileDesc d = A.desc[t];
+            const int row = d.r0 + (int)threadIdx.x;
+            if (row < d.r1) {
+                const double sv = dsub(V.r[row], dmul(a, V.v[row]));
+                V.s[row] = sv;
+                mb = umax(mb, absbits(sv));
+            }
+        }
+        mb = group_max<SM_NT / 32, 0>(mb, sm.redu);
+        if (threadIdx.x == 0 && mb) atomicMax(&maxslot[1], mb);
+        grid.sync();
+        // D: t = M s, t.t, t.s
+        for (int t = blockIdx.x; t < nt; t += gridDim.x) {
+            int row;
+            const double s = tile_rowsum_direct(A, t, V.s, sm, row);
+            double p1 = 0.0, p2 = 0.0;
+            if (row >= 0) { V.t[row] = s; p1 = dmul(s, s); p2 = dmul(s, V.s[row]); }
+            p1 = group_sum<SM_NT / 32, 0>(p1, sm.red);
+            p2 = group_sum<SM_NT / 32, 0>(p2, sm.red);
+            if (threadIdx.x == 0) { V.P1[t] = p1; V.P2[t] = p2; }
+        }
+        grid.sync();
+        const bool small = read_max(&maxslot[1]) <= tol;
+        const double tt = all_reduce_partials(V.P1, nt, sm.red);
+        const double ts = all_reduce_partials(V.P2, nt, sm.red);
+        if (tiny(tt)) {
+            if (!small) { stop = BREAKDOWN; which = 3; bd_it = cur; break; }
+            w = 0.0;
+        } else {
+            w = ddiv(ts, tt);
+        }
+        // E: x += a p + w s, r = s - w t, q.r
+        for (int t = blockIdx.x; t < nt; t += gridDim.x) {
+            const TileDesc d = A.desc[t];
+            const int row = d.r0 + (int)threadIdx.x;
+            double p1 = 0.0;
+            if (row < d.r1) {
+                const double sv = V.s[row];
+                V.x[row] = dadd(dadd(V.x[row], dmul(a, V.p[row])), dmul(w, sv));
+                const double rv = dsub(sv, dmul(w, V.t[row]));
+                V.r[row] = rv;
+                p1 = dmul(V.q[row], rv);
+            }
+            p1 = group_sum<SM_NT / 32, 0>(p1, sm.red);
+            if (threadIdx.x == 0) V.P1[t] = p1;
+        }
+        grid.sync();
+        it = cur;
+        if (small) { stop = CONVERGED; break; }
+        if (it >= max_it) { stop = NOTCONV; break; }
+        const double qr = all_reduce_partials(V.P1, nt, sm.red);
+        const double denom = dmul(y, w);
+        y = qr;
+        if (tiny(denom)) { stop = BREAKDOWN; which = 1; bd_it = it + 1; break; }
+        beta = ddiv(dmul(qr, a), denom);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        st->it = it;
+        st->stop = stop;
+        st->which = which;
+        st->bd_it = bd_it;
+    }
+}
+
 // ---------------------------------------------------------------- element-wise phases
 // BiCGStab vector updates, CHUNK_PER rows per thread (rows strided by CHUNK_NT: coalesced).
 template <int PH>
@@ -726,6 +984,8 @@ __global__ void __launch_bounds__(CHUNK_NT) k_phase(Vecs V, int n, SolveState* s
     __shared__ double s_red[CHUNK_NT / 32];
     __shared__ unsigned long long s_redu[CHUNK_NT / 32];
     __shared__ int s_flag;
+    griddep_wait();
+    griddep_launch();
     if (st->stop) return;
     const int base = blockIdx.x * CHUNK_ROWS + threadIdx.x;
     if constexpr (PH == PH_A) {
@@ -810,6 +1070,8 @@ template <int W>
 __global__ void __launch_bounds__(SEQ_NT) k_seqdot(Vecs V, int n, SolveState* st) {
     __shared__ double buf[2][2][SEQ_BLK];
     __shared__ double s_acc2;
+    griddep_wait();
+    griddep_launch();
     if (st->stop) return;
     const double* u1 = (W == SQ_T) ? V.t : V.q;
     const double* v1 = (W == SQ_S0 || W == SQ_E) ? V.r : (W == SQ_V ? V.v : V.t);
@@ -866,6 +1128,8 @@ __global__ void __launch_bounds__(32) k_dense(const double* __restrict__ A, int 
     extern __shared__ __align__(128) double dsm[];
     __shared__ __align__(8) uint64_t bars[DSTAGES];
     __shared__ int s_flag;
+    griddep_wait();
+    griddep_launch();
     if constexpr (epi_checks_stop<EPI>()) {
         if (st->stop) return;
     }

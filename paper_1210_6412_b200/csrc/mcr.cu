@@ -106,6 +106,8 @@ struct mcr_matrix {
     int64_t bytes = 0;
     int seqdots = 0;
     int spmv_grid = 1;
+    int small_grid = 0;                     // > 0: whole solve in one cooperative launch
+    unsigned long long* maxslot = nullptr;  // 3 slots for the persistent solvers
     std::mutex mu;
 
     double* vec(int k) const { return work + (size_t)k * (size_t)n; }
@@ -182,7 +184,7 @@ Vecs base_vecs(const mcr_matrix* h) {
 int ensure_work(mcr_matrix* h) {
     if (h->work) return MCR_OK;
     TRY(dalloc(h, &h->work, (size_t)V_COUNT * (size_t)h->n));
-    h->nunits = std::max({h->ntiles, h->nchunks(), h->nslabs, h->sell.nwin, 1});
+    h->nunits = std::max({h->ntiles, h->nchunks(), h->nslabs, h->sell.nwin * (SELL_W / SELL_CTA), 1});
     TRY(dalloc(h, &h->P, (size_t)2 * h->nunits));
     return MCR_OK;
 }
@@ -293,31 +295,50 @@ int read_state(mcr_matrix* h) {
 }
 
 // ---------------------------------------------------------------- kernel launchers
+// Every solve kernel goes out with programmatic stream serialization (PDL): the next kernel
+// of the chain is scheduled while the current one drains, and waits in griddepcontrol.wait.
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem,
+                cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 template <int EPI>
 void launch_mv(mcr_matrix* h, bool offdiag, const double* x, const Vecs& V, int64_t* launches) {
     if (h->storage == MCR_STORAGE_DENSE) {
-        k_dense<EPI><<<h->nslabs, 32, DENSE_SMEM, h->stream>>>(h->dense, (int)h->n, x, V, h->st);
+        launch_pdl(k_dense<EPI>, h->nslabs, 32, DENSE_SMEM, h->stream, (const double*)h->dense,
+                   (int)h->n, x, V, h->st);
     } else if (h->use_sell) {
         const auto& S = offdiag ? h->rsell : h->sell;
-        k_sell<EPI><<<S.nwin, SELL_W, 0, h->stream>>>(Sell{S.sptr, S.perm, S.col, S.val, S.nwin},
-                                                       x, V, h->st);
+        launch_pdl(k_sell<EPI>, S.nwin * (SELL_W / SELL_CTA), SELL_CTA, 0, h->stream,
+                   Sell{S.sptr, S.perm, S.col, S.val, S.nwin}, x, V, h->st);
     } else {
-        k_spmv<EPI><<<h->spmv_grid, SP_THREADS, SP_SMEM, h->stream>>>(
-            offdiag ? csr_off(h) : csr_full(h), x, V, h->st);
+        launch_pdl(k_spmv<EPI>, h->spmv_grid, SP_THREADS, SP_SMEM, h->stream,
+                   offdiag ? csr_off(h) : csr_full(h), x, V, h->st);
     }
     ++*launches;
 }
 
 template <int PH>
 void launch_phase(mcr_matrix* h, const Vecs& V, int64_t* launches) {
-    k_phase<PH><<<h->nchunks(), CHUNK_NT, 0, h->stream>>>(V, (int)h->n, h->st);
+    launch_pdl(k_phase<PH>, h->nchunks(), CHUNK_NT, 0, h->stream, V, (int)h->n, h->st);
     ++*launches;
 }
 
 template <int W>
 void launch_seqdot(mcr_matrix* h, const Vecs& V, int64_t* launches) {
     if (!h->seqdots) return;
-    k_seqdot<W><<<1, SEQ_NT, 0, h->stream>>>(V, (int)h->n, h->st);
+    launch_pdl(k_seqdot<W>, 1, SEQ_NT, 0, h->stream, V, (int)h->n, h->st);
     ++*launches;
 }
 
@@ -357,7 +378,14 @@ int jacobi_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double tol
     CK(cudaEventRecord(h->ev0, h->stream));
     int64_t launched = 0, sweeps = 0;
     int batch = 4;
-    for (;;) {
+    if (h->small_grid > 0) {
+        CK(cudaMemsetAsync(h->maxslot, 0, 3 * sizeof(unsigned long long), h->stream));
+        Csr R = csr_off(h);
+        void* args[] = {&R, &V, &h->st, &h->maxslot};
+        CK(cudaLaunchCooperativeKernel((void*)k_jacobi_small, h->small_grid, SM_NT, args, 0, h->stream));
+        ++launched;
+        TRY(read_state(h));
+    } else for (;;) {
         const int k = (int)std::min<int64_t>(batch, max_it - sweeps);
         for (int i = 0; i < k; ++i) launch_mv<EPI_JACOBI>(h, true, nullptr, V, &launched);
         CK(cudaGetLastError());
@@ -395,11 +423,21 @@ int bicgstab_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double t
     Vecs V = base_vecs(h);
     CK(cudaEventRecord(h->ev0, h->stream));
     int64_t launched = 0, iters = 0;
-    launch_mv<EPI_S0>(h, false, V.x, V, &launched);  // r = b - 1.0 * M x0, q = r, p = v = 0
-    launch_seqdot<SQ_S0>(h, V, &launched);
-    CK(cudaGetLastError());
-    TRY(read_state(h));
     int batch = 4;
+    if (h->small_grid > 0 && !h->seqdots) {
+        CK(cudaMemsetAsync(h->maxslot, 0, 3 * sizeof(unsigned long long), h->stream));
+        Csr A = csr_full(h);
+        void* args[] = {&A, &V, &h->st, &h->maxslot};
+        CK(cudaLaunchCooperativeKernel((void*)k_bicg_small, h->small_grid, SM_NT, args, 0, h->stream));
+        ++launched;
+        TRY(read_state(h));
+        iters = max_it;  // the loop below has nothing left to do
+    } else {
+        launch_mv<EPI_S0>(h, false, V.x, V, &launched);  // r = b - 1.0 * M x0, q = r, p = v = 0
+        launch_seqdot<SQ_S0>(h, V, &launched);
+        CK(cudaGetLastError());
+        TRY(read_state(h));
+    }
     while (!h->h_st->stop && iters < max_it) {
         const int k = (int)std::min<int64_t>(batch, max_it - iters);
         for (int i = 0; i < k; ++i) {
@@ -500,7 +538,7 @@ MCR_API void mcr_matrix_destroy(mcr_matrix* h) {
                             h->rrp, h->rcol, h->rval, h->dense, h->d, h->work, h->P, h->st,
                             h->sell.sptr, h->sell.perm, h->sell.col, h->sell.val, h->sell.swidth,
                             h->rsell.sptr, h->rsell.perm, h->rsell.col, h->rsell.val,
-                            h->rsell.swidth};
+                            h->rsell.swidth, h->maxslot};
             for (void* p : ptrs)
                 if (p) cudaFreeAsync(p, s);
             cudaStreamSynchronize(s);
@@ -615,6 +653,15 @@ static int create_impl(mcr_matrix* h, int64_t n, const int64_t* rs, const int64_
         CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv<EPI_V>, SP_THREADS, SP_SMEM));
         h->spmv_grid = std::max(1, std::min(h->ntiles, sms * std::max(per_sm, 1)));
+        int pj = 0, pb = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pj, k_jacobi_small, SM_NT, 0));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pb, k_bicg_small, SM_NT, 0));
+        const int coresident = sms * std::min(pj, pb);
+        // one tile per CTA keeps the per-sweep critical path to a single tile
+        if (!h->use_sell && storage != MCR_STORAGE_TILES_STREAM && h->ntiles <= coresident &&
+            h->ntiles <= 2 * sms)
+            h->small_grid = h->ntiles;
+        TRY(dalloc(h, &h->maxslot, 3));
         TRY(dalloc(h, &h->tile_row, tiles.size()));
         CK(cudaMemcpyAsync(h->tile_row, tiles.data(), sizeof(int) * tiles.size(),
                            cudaMemcpyHostToDevice, h->stream));

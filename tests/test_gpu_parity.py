@@ -119,29 +119,44 @@ def test_c2_bicgstab_tree_dots(gs):
 # ------------------------------------------------------------------ storage variants
 
 @pytest.mark.parametrize("name", ["kat_golden2x2", "kat_identity4", "kat_divergent",
-                                  "grid_20_9", "grid_50_5", "dense_1024", "c1_seed77"])
-@pytest.mark.parametrize("storage", [2, 3, 4])
+                                  "grid_20_9", "grid_50_5", "dense_1024", "c1_seed77",
+                                  "chain_random2", "c4_7647_15293", "seeded_guess"])
+@pytest.mark.parametrize("storage", [2, 3, 4, 5])
 def test_forced_storage_matches_reference(gs, name, storage):
-    """Dense slabs (2), SELL-32-sigma (3) and TMA-staged CSR tiles (4) give the same bits."""
+    """Dense slabs (2), SELL-32-sigma (3), CSR tiles solved in one cooperative launch (4) and
+    CSR tiles through the per-iteration TMA-pipelined kernels (5) give the same bits."""
     from paper_1210_6412_b200._lib import MCR_OK, MCR_NOT_CONVERGED
     m, b = system(name)
     dm = gs.DeviceMatrix(m, 0, storage)
     try:
-        assert dm.info()["storage"] == storage
+        assert dm.info()["storage"] == min(storage, 4)
+        def x0(cfg):
+            g = cfg["guess_seed"]
+            return None if g is None else np.random.default_rng(g).random(m.n)
+
         exp = expected(name, "jacobi")
         if exp["outcome"] in ("ok", "not_converged"):
             cfg = exp["config"]
-            rc, x, rep = dm.solve("jacobi", b, None, cfg["tolerance"], cfg["max_iterations"])
+            rc, x, rep = dm.solve("jacobi", b, x0(cfg), cfg["tolerance"], cfg["max_iterations"])
             assert rc in (MCR_OK, MCR_NOT_CONVERGED)
             assert rep.iterations == exp["iterations"]
             assert np.array_equal(x, exp["x"])
+            assert float(rep.residual_inf).hex() == exp["residual_inf"]
         exp = expected(name, "bicgstab")
         if exp["outcome"] == "ok":
             cfg = exp["config"]
-            rc, x, rep = dm.solve("bicgstab", b, None, cfg["tolerance"], cfg["max_iterations"])
+            rc, x, rep = dm.solve("bicgstab", b, x0(cfg), cfg["tolerance"], cfg["max_iterations"])
             assert rc == MCR_OK
-            assert abs(rep.iterations - exp["iterations"]) <= 1
+            # each storage reduces the inner products in its own (fixed) tree shape; the
+            # stopping iteration of BiCGStab moves with the summation order (e.g. c4_7647 dense
+            # slabs: 45 vs the reference's 48, tools/bicgstab_sensitivity.py); the
+            # sequential-dots solve below is the exact check
+            assert abs(rep.iterations - exp["iterations"]) <= 3
             assert rel_err(x, exp["x"]) <= REL_TOL
+            rc, x, rep = dm.solve("bicgstab", b, x0(cfg), cfg["tolerance"], cfg["max_iterations"],
+                                  dots="sequential")
+            assert rc == MCR_OK and rep.iterations == exp["iterations"]
+            assert np.array_equal(x, exp["x"])
         from oracle import oracle
         xr = np.random.default_rng(7).uniform(-3, 3, m.n)
         assert np.array_equal(dm.matvec(xr), oracle.spmv(m, xr))

@@ -13,7 +13,7 @@ elif cfg == "c1":
 elif cfg == "c3":
     n = 16384; seed = 3; spec = GenSpec(n=n, density=1.0, seed=seed)
 m = generate_dd_matrix(spec); b = generate_rhs(n, seed); nnz = m.m
-L = _lib.load(); dm = DeviceMatrix(m, 0)
+L = _lib.load(); dm = DeviceMatrix(m, 0, int(os.environ.get('MCR_STORAGE', '0')))
 s = torch.cuda.Stream(); L.mcr_set_stream(dm.handle, ctypes.c_void_p(s.cuda_stream))
 x = torch.rand(n, dtype=torch.float64, device="cuda"); y = torch.empty_like(x)
 flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.int32, device="cuda")
@@ -38,4 +38,4 @@ with torch.cuda.stream(s):
             rc = fn(dm.handle, ctypes.c_void_p(bd.data_ptr()), None, 1e-10, 10000, ctypes.c_void_p(xo.data_ptr()), ctypes.byref(rep))
             best = rep if best is None or rep.device_seconds < best.device_seconds else best
         res[name] = (rc, best.iterations, round(best.device_seconds * 1e3, 3), best.kernel_launches)
-print(os.environ.get("MCR_LIB", "default"), cfg, f"spmv {spmv*1e6:.1f}us {B/spmv/1e9:.0f}GB/s", res, flush=True)
+print(os.environ.get("MCR_LIB", "default"), os.environ.get("MCR_STORAGE", "0"), cfg, f"spmv {spmv*1e6:.1f}us {B/spmv/1e9:.0f}GB/s", res, flush=True)
