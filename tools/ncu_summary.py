@@ -19,7 +19,7 @@ KEYS = {
     "smem_bank_conflicts": "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
     "sm_clock_mhz": "smsp__cycles_elapsed.avg.per_second",
 }
-UNITS = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1,
+UNITS = {"ns": 1e-3, "us": 1.0, "ms": 1e3, "byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1,
          "msecond": 1e3, "second": 1e6, "hz": 1e-6, "Khz": 1e-3, "Mhz": 1, "Ghz": 1e3}
 
 
