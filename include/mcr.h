@@ -88,6 +88,10 @@ typedef struct mcr_matrix_info {
     int64_t max_row_nnz;
     int64_t first_zero_diagonal; /* -1 when every row has a non-zero diagonal               */
     int64_t device_bytes;        /* bytes of device memory held by the handle               */
+    int64_t n_global;            /* rows of the whole system (== n unless a row shard)       */
+    int64_t row0;                /* first global row held (0 unless a row shard)            */
+    int32_t world;               /* ranks the system is sharded over (1 = whole system)     */
+    int32_t rank;
 } mcr_matrix_info;
 
 /* Library version (major*10000 + minor*100 + patch). */
@@ -137,6 +141,36 @@ MCR_API int mcr_bicgstab(mcr_matrix* m, const double* b, const double* x0, doubl
 MCR_API int mcr_bicgstab_device(mcr_matrix* m, const double* d_b, const double* d_x0,
                                 double tol, int64_t max_iterations, double* d_x_out,
                                 mcr_report* report);
+
+/* ---------------------------------------------------------------------------------------
+ * Row-sharded solves over 1..N GPUs (the reference's row-block parallel
+ * solvers jacobi_solve_parallel / bicgstab_solve_parallel, solvers.py:159-168, 233-274,
+ * 314-396, with worker threads replaced by GPUs). Rank r of `world` holds the contiguous rows
+ * [r*c, min(n, (r+1)*c)), c = ceil(n / world) (mcr_shard_rows), as a local CSR whose column
+ * indices stay global. mcr_jacobi / mcr_bicgstab (and the _device variants) on a shard take
+ * and return this rank's slice of b, x0 and x; every rank must call the same solve with the
+ * same tolerance and iteration limit, and every rank gets the same iterations, residual and
+ * status. Jacobi iterates are bit-identical to the one-GPU (and reference) iterates.
+ * ------------------------------------------------------------------------------------- */
+#define MCR_COMM_ID_BYTES 128
+typedef struct mcr_comm mcr_comm;
+
+/* Contiguous row range of `rank`. */
+MCR_API int mcr_shard_rows(int64_t n_global, int world, int rank, int64_t* row0, int64_t* rows);
+/* NCCL bootstrap: rank 0 creates the id, the caller distributes it to every rank. */
+MCR_API int mcr_comm_unique_id(void* id);
+/* One process (or thread) per GPU; NCCL is loaded at run time (libnccl.so.2). */
+MCR_API int mcr_comm_create_nccl(const void* id, int world, int rank, int device, mcr_comm** out);
+/* `world` ranks of ONE process, each driven by its own host thread (devices[r], or device 0
+ * for all when devices is NULL): collectives become peer copies ordered by CUDA events. Fills
+ * out[0..world-1]. */
+MCR_API int mcr_comm_create_local(int world, const int* devices, mcr_comm** out);
+MCR_API void mcr_comm_destroy(mcr_comm* comm);
+MCR_API int mcr_comm_info(const mcr_comm* comm, int* world, int* rank, int* device);
+/* Upload this rank's rows (local rstart, GLOBAL columns) of an n_global x n_global system. */
+MCR_API int mcr_shard_create(mcr_comm* comm, int64_t n_global, int64_t row0, int64_t rows,
+                             const int64_t* rstart, const int64_t* col, const double* nonzero,
+                             mcr_matrix** out);
 
 /* Message of the last failing call on this thread ("" if none). */
 MCR_API const char* mcr_last_error(void);

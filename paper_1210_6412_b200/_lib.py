@@ -28,7 +28,10 @@ EXPORTS = (
     "mcr_matrix_info_get", "mcr_set_stream", "mcr_matvec", "mcr_matvec_device",
     "mcr_residual_inf", "mcr_jacobi", "mcr_jacobi_device", "mcr_bicgstab",
     "mcr_bicgstab_device", "mcr_last_error", "mcr_set_dot_mode",
+    "mcr_shard_rows", "mcr_comm_unique_id", "mcr_comm_create_nccl", "mcr_comm_create_local",
+    "mcr_comm_destroy", "mcr_comm_info", "mcr_shard_create",
 )
+COMM_ID_BYTES = 128
 DOTS_TREE, DOTS_SEQUENTIAL = 0, 1
 
 
@@ -59,6 +62,10 @@ class MatrixInfo(ctypes.Structure):
         ("max_row_nnz", ctypes.c_int64),
         ("first_zero_diagonal", ctypes.c_int64),
         ("device_bytes", ctypes.c_int64),
+        ("n_global", ctypes.c_int64),
+        ("row0", ctypes.c_int64),
+        ("world", ctypes.c_int32),
+        ("rank", ctypes.c_int32),
     ]
 
 
@@ -94,6 +101,17 @@ def load():
     L.mcr_residual_inf.argtypes = [vp, vp, vp, ctypes.POINTER(dbl)]
     for name in ("mcr_jacobi", "mcr_jacobi_device", "mcr_bicgstab", "mcr_bicgstab_device"):
         getattr(L, name).argtypes = [vp, vp, vp, dbl, i64, vp, ctypes.POINTER(Report)]
+    ip = ctypes.c_int
+    pi64 = ctypes.POINTER(i64)
+    pint = ctypes.POINTER(ctypes.c_int)
+    L.mcr_shard_rows.argtypes = [i64, ip, ip, pi64, pi64]
+    L.mcr_comm_unique_id.argtypes = [vp]
+    L.mcr_comm_create_nccl.argtypes = [vp, ip, ip, ip, ctypes.POINTER(vp)]
+    L.mcr_comm_create_local.argtypes = [ip, vp, ctypes.POINTER(vp)]
+    L.mcr_comm_destroy.argtypes = [vp]
+    L.mcr_comm_destroy.restype = None
+    L.mcr_comm_info.argtypes = [vp, pint, pint, pint]
+    L.mcr_shard_create.argtypes = [vp, i64, i64, i64, vp, vp, vp, ctypes.POINTER(vp)]
     L.mcr_last_error.restype = ctypes.c_char_p
     L.mcr_last_error.argtypes = []
     _lib = L

@@ -44,6 +44,7 @@ constexpr int CSR_PAD = 4;       // extra elements allocated behind rowptr / col
 constexpr double TINY = 1e-300;  // solvers.py:40
 
 enum Stop : int { RUNNING = 0, CONVERGED = 1, NOTCONV = 2, BREAKDOWN = 3 };
+constexpr int SEND_SLOTS = 4;    // doubles each rank contributes per reduction point
 
 // Device-resident solver state: all control flow of a solve lives here, so an iteration never
 // needs the host. Written only by the "last CTA" of a kernel (after every other CTA of that
@@ -61,6 +62,10 @@ struct SolveState {
     double y, a, w, beta, qv, tt, ts, resid;
     int small;
     int seqdots;  // 1: inner products by k_seqdot (reference order, bit-exact), not the tree
+    int sharded;  // 1: row shard of a multi-GPU system -- reduction kernels publish their local
+                  //    partials in send[] instead of finalising; k_finalize finishes after the
+                  //    per-rank exchange
+    double send[SEND_SLOTS];  // {dot 1, dot 2, max|.| as bits, unused} of this rank
 };
 
 // Entry range [e0, e1) and row range [r0, r1) of one tile.
@@ -94,8 +99,9 @@ struct Vecs {
     double* t;
     double* P1;          // per-unit partials
     double* P2;
-    double* x_jac0;      // Jacobi double buffer (for sweep parity)
+    double* x_jac0;      // Jacobi double buffer (for sweep parity); full length when sharded
     double* x_jac1;
+    long long roff;      // first global row of this shard (0 on one GPU): own slice of x_jac*
 };
 
 enum Epi : int { EPI_Y = 0, EPI_RESID = 1, EPI_JACOBI = 2, EPI_S0 = 3, EPI_V = 4, EPI_T = 5 };
@@ -378,6 +384,20 @@ __device__ __forceinline__ void kernel_finish(const Vecs& V, SolveState* st, int
     }
     if constexpr (EPI == EPI_Y && !PERSISTENT) return;  // nothing to finalise
     if (!last_cta(&st->done, s_flag)) return;
+    if (st->sharded) {  // publish this rank's partials; k_finalize runs after the exchange
+        double r1 = 0.0, r2 = 0.0;
+        if constexpr (epi_has_dot<EPI>()) r1 = reduce_partials<NT>(V.P1, nunits, s_red);
+        if constexpr (EPI == EPI_T) r2 = reduce_partials<NT>(V.P2, nunits, s_red);
+        if (threadIdx.x == 0) {
+            st->send[0] = r1;
+            st->send[1] = r2;
+            st->send[2] = bits2d(atomicExch(&st->maxbits, 0ull));
+            st->send[3] = 0.0;
+            st->done = 0;
+            st->tile_ctr = 0;
+        }
+        return;
+    }
     if constexpr (epi_has_dot<EPI>()) {
         if (st->seqdots) {  // k_seqdot runs the reference-order dots and finalises
             if (threadIdx.x == 0) { st->done = 0; st->tile_ctr = 0; }
@@ -411,9 +431,10 @@ template <int EPI>
 __device__ __forceinline__ const double* jacobi_select(const double* x, Vecs& V, SolveState* st) {
     if constexpr (EPI == EPI_JACOBI) {
         const long long it = st->it + 1;  // sweep it reads buffer (it+1)&1, writes it&1
-        V.xcur = (it & 1) ? V.x_jac0 : V.x_jac1;
-        V.xnext = (it & 1) ? V.x_jac1 : V.x_jac0;
-        return V.xcur;
+        const double* cur = (it & 1) ? V.x_jac0 : V.x_jac1;
+        V.xcur = cur + V.roff;          // own rows (the whole vector on one GPU)
+        V.xnext = ((it & 1) ? V.x_jac1 : V.x_jac0) + V.roff;
+        return cur;                     // gathers read the full (allgathered) iterate
     }
     return x;
 }
@@ -1053,6 +1074,13 @@ __global__ void __launch_bounds__(CHUNK_NT) k_phase(Vecs V, int n, SolveState* s
         const double qr = reduce_partials<CHUNK_NT>(V.P1, gridDim.x, s_red);
         if (threadIdx.x != 0) return;
         st->done = 0;
+        if (st->sharded) {
+            st->send[0] = qr;
+            st->send[1] = 0.0;
+            st->send[2] = 0.0;
+            st->send[3] = 0.0;
+            return;
+        }
         fin_e(st, qr);
     }
 }
@@ -1114,6 +1142,44 @@ __global__ void __launch_bounds__(SEQ_NT) k_seqdot(Vecs V, int n, SolveState* st
     else if constexpr (W == SQ_V) fin_v(st, acc);
     else if constexpr (W == SQ_T) fin_t(st, acc, s_acc2);
     else fin_e(st, acc);
+}
+
+// ---------------------------------------------------------------- multi-GPU reduction points
+// After the per-rank exchange every rank holds the same `world` x SEND_SLOTS partials; one
+// thread sums the dots in ascending rank order and takes the max, then runs the same scalar
+// step as the single-GPU path. Identical inputs -> identical bits -> every rank takes the same
+// stop / breakdown decision with no further communication.
+enum FinWhich : int { FIN_JACOBI = 0, FIN_RESID = 1, FIN_S0 = 2, FIN_V = 3, FIN_T = 4, FIN_E = 5 };
+
+template <int W>
+__global__ void k_finalize(SolveState* st, const double* __restrict__ recv, int world) {
+    griddep_wait();
+    griddep_launch();
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (W != FIN_RESID && st->stop) return;
+    double d1 = 0.0, d2 = 0.0;
+    unsigned long long mb = 0;
+    for (int r = 0; r < world; ++r) {
+        d1 = dadd(d1, recv[r * SEND_SLOTS + 0]);
+        d2 = dadd(d2, recv[r * SEND_SLOTS + 1]);
+        mb = umax(mb, (unsigned long long)__double_as_longlong(recv[r * SEND_SLOTS + 2]));
+    }
+    if constexpr (W == FIN_JACOBI) {
+        const double md = bits2d(mb);
+        const long long it = st->it + 1;
+        st->it = it;
+        if (md <= st->tol) st->stop = CONVERGED;
+        else if (it >= st->max_it) st->stop = NOTCONV;
+    } else if constexpr (W == FIN_RESID) {
+        st->resid = bits2d(mb);
+    } else {
+        st->maxbits = mb;  // read (and cleared) by fin_s0 / fin_t
+        if constexpr (W == FIN_S0) fin_s0(st, d1);
+        else if constexpr (W == FIN_V) fin_v(st, d1);
+        else if constexpr (W == FIN_T) fin_t(st, d1, d2);
+        else fin_e(st, d1);
+        st->maxbits = 0ull;
+    }
 }
 
 // ---------------------------------------------------------------- dense slab GEMV (TMA bulk)
@@ -1215,20 +1281,22 @@ __global__ void k_col64to32(const long long* __restrict__ in, int* __restrict__ 
 }
 
 // Stored diagonal per row (0.0 if absent; rows sorted -> binary search), the off-diagonal
-// row length, and the first row whose diagonal is 0 (ZeroDiagonal).
+// row length, and the first row whose diagonal is 0 (ZeroDiagonal). Row i of the handle is
+// global row roff + i (row shards keep global column indices).
 __global__ void k_diag(const long long* __restrict__ rp, const int* __restrict__ col,
-                       const double* __restrict__ val, int n, double* d, long long* offlen,
-                       unsigned long long* first_zero) {
+                       const double* __restrict__ val, int n, long long roff, double* d,
+                       long long* offlen, unsigned long long* first_zero) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         long long lo = rp[i], hi = rp[i + 1];
         const long long len = hi - lo;
+        const long long gi = roff + i;
         double dv = 0.0;
         int has = 0;
         while (lo < hi) {
             const long long mid = (lo + hi) >> 1;
-            const int c = col[mid];
-            if (c == i) { dv = val[mid]; has = 1; break; }
-            if (c < i) lo = mid + 1; else hi = mid;
+            const long long c = col[mid];
+            if (c == gi) { dv = val[mid]; has = 1; break; }
+            if (c < gi) lo = mid + 1; else hi = mid;
         }
         d[i] = dv;
         if (offlen) offlen[i] = len - has;
@@ -1239,7 +1307,7 @@ __global__ void k_diag(const long long* __restrict__ rp, const int* __restrict__
 // Off-diagonal copy R (without_diagonal, sparse.py:227-231): order of the kept entries is
 // unchanged. One warp per row.
 __global__ void k_split_offdiag(const long long* __restrict__ rp, const int* __restrict__ col,
-                                const double* __restrict__ val, int n,
+                                const double* __restrict__ val, int n, long long roff,
                                 const long long* __restrict__ rrp, int* rcol, double* rval) {
     const int lane = threadIdx.x & 31;
     const int warps = (gridDim.x * blockDim.x) >> 5;
@@ -1250,7 +1318,7 @@ __global__ void k_split_offdiag(const long long* __restrict__ rp, const int* __r
             const long long k = k0 + lane;
             const bool inr = k < e;
             const int c = inr ? col[k] : -1;
-            const bool keep = inr && c != i;
+            const bool keep = inr && (long long)c != roff + i;
             const unsigned msk = __ballot_sync(0xffffffffu, keep);
             if (keep) {
                 const long long pos = out + __popc(msk & ((1u << lane) - 1u));

@@ -20,6 +20,7 @@
 
 #include <cub/device/device_scan.cuh>
 
+#include "comm.h"
 #include "device.cuh"
 #include "mcr.h"
 
@@ -54,13 +55,27 @@ struct DeviceGuard {
     }
 };
 
-enum { V_B = 0, V_X, V_X1, V_R, V_Q, V_P, V_V, V_S, V_T, V_COUNT };
+// Work vectors. FULL ones are gather inputs of the SpMV and span the whole system when the
+// matrix is a row shard (world * chunk entries, indexed by global row); the others hold this
+// handle's rows only. On one GPU both kinds are n long.
+enum { V_X = 0, V_X1, V_P, V_S, V_FULL_COUNT, V_B = V_FULL_COUNT, V_R, V_Q, V_V, V_T, V_COUNT };
 
 }  // namespace
 
+// Communicator of a row-sharded solve (comm.h): NCCL, or the in-process local group.
+struct mcr_comm {
+    std::shared_ptr<mcr::Transport> t;
+};
+
 struct mcr_matrix {
     int device = 0;
-    int64_t n = 0, nnz = 0;
+    int64_t n = 0, nnz = 0;           // rows (and entries) held by this handle
+    // row sharding: this handle holds rows [roff, roff + n) of an n_global system; every rank
+    // holds `chunk` = ceil(n_global / world) rows except the last
+    int world = 1, rank = 0;
+    int64_t n_global = 0, roff = 0, chunk = 0;
+    std::shared_ptr<Transport> comm;
+    double* recv = nullptr;           // world * SEND_SLOTS exchanged partials
     int storage = MCR_STORAGE_CSR;
     cudaStream_t own_stream = nullptr, stream = nullptr;
     // full matrix, CSR
@@ -110,7 +125,15 @@ struct mcr_matrix {
     unsigned long long* maxslot = nullptr;  // 3 slots for the persistent solvers
     std::mutex mu;
 
-    double* vec(int k) const { return work + (size_t)k * (size_t)n; }
+    int64_t n_full() const { return comm ? chunk * world : n; }
+    double* vec(int k) const {
+        return k < V_FULL_COUNT ? work + (size_t)k * (size_t)n_full()
+                                : work + (size_t)V_FULL_COUNT * (size_t)n_full() +
+                                      (size_t)(k - V_FULL_COUNT) * (size_t)n;
+    }
+    // a row shard (mcr_shard_create) runs the exchange points even at world 1, so the NCCL
+    // transport is exercised end to end on a one-GPU box
+    bool sharded() const { return comm != nullptr; }
     int nchunks() const { return (int)((n + CHUNK_ROWS - 1) / CHUNK_ROWS); }
 };
 
@@ -163,29 +186,38 @@ Csr csr_off(const mcr_matrix* h) {
     return Csr{h->rrp, h->rcol, h->rval, h->rdesc, h->ntiles, (int)h->n};
 }
 
+// Own-row views (x, p, s point at this rank's slice of the full vectors).
 Vecs base_vecs(const mcr_matrix* h) {
     Vecs V{};
     V.b = h->vec(V_B);
     V.d = h->d;
-    V.x = h->vec(V_X);
+    V.x = h->vec(V_X) + h->roff;
     V.r = h->vec(V_R);
     V.q = h->vec(V_Q);
-    V.p = h->vec(V_P);
+    V.p = h->vec(V_P) + h->roff;
     V.v = h->vec(V_V);
-    V.s = h->vec(V_S);
+    V.s = h->vec(V_S) + h->roff;
     V.t = h->vec(V_T);
     V.P1 = h->P;
     V.P2 = h->P + h->nunits;
     V.x_jac0 = h->vec(V_X);
     V.x_jac1 = h->vec(V_X1);
+    V.roff = h->roff;
     return V;
 }
 
 int ensure_work(mcr_matrix* h) {
     if (h->work) return MCR_OK;
-    TRY(dalloc(h, &h->work, (size_t)V_COUNT * (size_t)h->n));
+    const size_t words = (size_t)V_FULL_COUNT * (size_t)h->n_full() +
+                         (size_t)(V_COUNT - V_FULL_COUNT) * (size_t)h->n;
+    TRY(dalloc(h, &h->work, words));
+    // full vectors start zeroed: blocks past the last rank's rows are gathered but never read
+    if (h->sharded())
+        CK(cudaMemsetAsync(h->work, 0, sizeof(double) * (size_t)V_FULL_COUNT * (size_t)h->n_full(),
+                           h->stream));
     h->nunits = std::max({h->ntiles, h->nchunks(), h->nslabs, h->sell.nwin * (SELL_W / SELL_CTA), 1});
     TRY(dalloc(h, &h->P, (size_t)2 * h->nunits));
+    if (h->sharded()) TRY(dalloc(h, &h->recv, (size_t)h->world * SEND_SLOTS));
     return MCR_OK;
 }
 
@@ -242,8 +274,8 @@ int ensure_offdiag(mcr_matrix* h) {
     const int threads = 256;
     const int blocks = (int)std::min<long long>(((long long)n * 32 + threads - 1) / threads, 1 << 20);
     if (n > 0)
-        k_split_offdiag<<<blocks, threads, 0, h->stream>>>(h->rp, h->col, h->val, n, h->rrp,
-                                                           h->rcol, h->rval);
+        k_split_offdiag<<<blocks, threads, 0, h->stream>>>(h->rp, h->col, h->val, n, h->roff,
+                                                           h->rrp, h->rcol, h->rval);
     CK(cudaGetLastError());
     TRY(dalloc(h, &h->rdesc, (size_t)h->ntiles));
     if (h->ntiles > 0)
@@ -286,6 +318,7 @@ void set_state(mcr_matrix* h, double tol, int64_t max_it) {
     s.max_it = max_it;
     s.y = s.a = s.w = 1.0;
     s.seqdots = h->seqdots;
+    s.sharded = h->sharded() ? 1 : 0;
 }
 
 int read_state(mcr_matrix* h) {
@@ -342,34 +375,95 @@ void launch_seqdot(mcr_matrix* h, const Vecs& V, int64_t* launches) {
     ++*launches;
 }
 
-int residual_into_state(mcr_matrix* h, const double* x, int64_t* launches) {
-    Vecs V = base_vecs(h);
-    launch_mv<EPI_RESID>(h, false, x, V, launches);
+// ---------------------------------------------------------------- sharded exchange points
+// One reduction point of a row-sharded solve: every rank's SEND_SLOTS partials (written by
+// the producing kernel's last CTA into st->send) are exchanged, then k_finalize<W> reduces them
+// in rank order and takes the scalar step. `buf` != null also allgathers that full vector in
+// the same step (Jacobi: the iterate just written).
+template <int W>
+int exchange_point(mcr_matrix* h, double* buf, int64_t* launches) {
+    Transport& T = *h->comm;
+    const double* send = h->st->send;
+    const int rc = buf ? T.allgather_and_slots(buf, (size_t)h->chunk, send, h->recv, SEND_SLOTS,
+                                               h->stream)
+                       : T.gather_slots(send, h->recv, SEND_SLOTS, h->stream);
+    if (rc) return fail(MCR_CUDA_ERROR, std::string(T.kind()) + " exchange: " + T.err);
+    launch_pdl(k_finalize<W>, 1, 32, 0, h->stream, h->st, (const double*)h->recv, h->world);
+    ++*launches;
     CK(cudaGetLastError());
     return MCR_OK;
 }
 
+int allgather_full(mcr_matrix* h, double* buf) {
+    Transport& T = *h->comm;
+    if (T.allgather(buf, (size_t)h->chunk, h->stream))
+        return fail(MCR_CUDA_ERROR, std::string(T.kind()) + " allgather: " + T.err);
+    return MCR_OK;
+}
+
+// max|b - M x| into st->resid; x is the full (gathered) vector.
+int residual_into_state(mcr_matrix* h, const double* x, int64_t* launches) {
+    Vecs V = base_vecs(h);
+    launch_mv<EPI_RESID>(h, false, x, V, launches);
+    CK(cudaGetLastError());
+    if (h->sharded()) TRY(exchange_point<FIN_RESID>(h, nullptr, launches));
+    return MCR_OK;
+}
+
+// b -> V_B; x0 (this handle's rows) -> own slice of the full vector `x0_slot`, gathered when
+// sharded; no x0 means zeros.
 int prepare_inputs(mcr_matrix* h, const double* d_b, const double* d_x0, int x0_slot) {
     const size_t bytes = sizeof(double) * (size_t)h->n;
     CK(cudaMemcpyAsync(h->vec(V_B), d_b, bytes, cudaMemcpyDeviceToDevice, h->stream));
-    if (d_x0)
-        CK(cudaMemcpyAsync(h->vec(x0_slot), d_x0, bytes, cudaMemcpyDeviceToDevice, h->stream));
-    else
-        CK(cudaMemsetAsync(h->vec(x0_slot), 0, bytes, h->stream));
+    double* full = h->vec(x0_slot);
+    if (d_x0) {
+        CK(cudaMemcpyAsync(full + h->roff, d_x0, bytes, cudaMemcpyDeviceToDevice, h->stream));
+        if (h->sharded()) TRY(allgather_full(h, full));
+    } else {
+        CK(cudaMemsetAsync(full, 0, sizeof(double) * (size_t)h->n_full(), h->stream));
+    }
+    return MCR_OK;
+}
+
+// ZeroDiagonal must be decided identically on every rank before any sweep (a rank that
+// returned early would leave its peers waiting in a collective): exchange each rank's first
+// zero-diagonal row and take the smallest.
+int global_first_zero(mcr_matrix* h, long long* out) {
+    if (!h->sharded()) {
+        *out = h->first_zero;
+        return MCR_OK;
+    }
+    double mine[SEND_SLOTS] = {(double)h->first_zero, 0.0, 0.0, 0.0};
+    CK(cudaMemcpyAsync(h->st->send, mine, sizeof(mine), cudaMemcpyHostToDevice, h->stream));
+    Transport& T = *h->comm;
+    if (T.gather_slots(h->st->send, h->recv, SEND_SLOTS, h->stream))
+        return fail(MCR_CUDA_ERROR, std::string(T.kind()) + " exchange: " + T.err);
+    std::vector<double> all((size_t)h->world * SEND_SLOTS);
+    CK(cudaMemcpyAsync(all.data(), h->recv, sizeof(double) * all.size(), cudaMemcpyDeviceToHost,
+                       h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    long long best = -1;
+    for (int r = 0; r < h->world; ++r) {
+        const long long z = (long long)all[(size_t)r * SEND_SLOTS];
+        if (z >= 0 && (best < 0 || z < best)) best = z;
+    }
+    *out = best;
     return MCR_OK;
 }
 
 // Batches grow 4, 8, ..., 32: a batch that overshoots the stop point only launches kernels
-// that return at their first instruction.
+// that return at their first instruction (and, sharded, exchanges that rewrite unchanged data).
 int next_batch(int cur) { return std::min(cur * 2, 32); }
 
 int jacobi_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double tol, int64_t max_it,
                 double* d_x_out, mcr_report* rep) {
-    if (h->first_zero >= 0) {
-        rep->zero_diagonal_index = h->first_zero;
-        return fail(MCR_ZERO_DIAGONAL, "zero diagonal entry in row " + std::to_string(h->first_zero));
-    }
     TRY(ensure_work(h));
+    long long zero = -1;
+    TRY(global_first_zero(h, &zero));
+    if (zero >= 0) {
+        rep->zero_diagonal_index = zero;
+        return fail(MCR_ZERO_DIAGONAL, "zero diagonal entry in row " + std::to_string(zero));
+    }
     TRY(ensure_offdiag(h));
     TRY(prepare_inputs(h, d_b, d_x0, V_X));
     set_state(h, tol, max_it);
@@ -387,7 +481,14 @@ int jacobi_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double tol
         TRY(read_state(h));
     } else for (;;) {
         const int k = (int)std::min<int64_t>(batch, max_it - sweeps);
-        for (int i = 0; i < k; ++i) launch_mv<EPI_JACOBI>(h, true, nullptr, V, &launched);
+        for (int i = 0; i < k; ++i) {
+            launch_mv<EPI_JACOBI>(h, true, nullptr, V, &launched);
+            if (h->sharded()) {  // sweep s writes buffer s & 1: gather it with the partial max
+                const int64_t sweep = sweeps + i + 1;
+                TRY(exchange_point<FIN_JACOBI>(h, (sweep & 1) ? h->vec(V_X1) : h->vec(V_X),
+                                               &launched));
+            }
+        }
         CK(cudaGetLastError());
         sweeps += k;
         TRY(read_state(h));
@@ -395,15 +496,15 @@ int jacobi_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double tol
         batch = next_batch(batch);
     }
     const long long it = h->h_st->it;
-    const double* x = (it & 1) ? h->vec(V_X1) : h->vec(V_X);
+    const double* x = (it & 1) ? h->vec(V_X1) : h->vec(V_X);  // full iterate (gathered)
     TRY(residual_into_state(h, x, &launched));
     CK(cudaEventRecord(h->ev1, h->stream));
     TRY(read_state(h));
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
     if (d_x_out)
-        CK(cudaMemcpyAsync(d_x_out, x, sizeof(double) * (size_t)h->n, cudaMemcpyDeviceToDevice,
-                           h->stream));
+        CK(cudaMemcpyAsync(d_x_out, x + h->roff, sizeof(double) * (size_t)h->n,
+                           cudaMemcpyDeviceToDevice, h->stream));
     CK(cudaStreamSynchronize(h->stream));
     const SolveState& s = *h->h_st;
     rep->iterations = s.it;
@@ -421,6 +522,7 @@ int bicgstab_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double t
     set_state(h, tol, max_it);
     CK(cudaMemcpyAsync(h->st, h->h_st, sizeof(SolveState), cudaMemcpyHostToDevice, h->stream));
     Vecs V = base_vecs(h);
+    const bool sh = h->sharded();
     CK(cudaEventRecord(h->ev0, h->stream));
     int64_t launched = 0, iters = 0;
     int batch = 4;
@@ -433,29 +535,39 @@ int bicgstab_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double t
         TRY(read_state(h));
         iters = max_it;  // the loop below has nothing left to do
     } else {
-        launch_mv<EPI_S0>(h, false, V.x, V, &launched);  // r = b - 1.0 * M x0, q = r, p = v = 0
+        // r = b - 1.0 * M x0, q = r, p = v = 0
+        launch_mv<EPI_S0>(h, false, h->vec(V_X), V, &launched);
         launch_seqdot<SQ_S0>(h, V, &launched);
         CK(cudaGetLastError());
+        if (sh) TRY(exchange_point<FIN_S0>(h, nullptr, &launched));
         TRY(read_state(h));
     }
+    double* p_full = h->vec(V_P);
+    double* s_full = h->vec(V_S);
     while (!h->h_st->stop && iters < max_it) {
         const int k = (int)std::min<int64_t>(batch, max_it - iters);
         for (int i = 0; i < k; ++i) {
             launch_phase<PH_A>(h, V, &launched);               // p = r + beta (p - w v)
-            launch_mv<EPI_V>(h, false, V.p, V, &launched);     // v = M p, q.v -> a
+            if (sh) TRY(allgather_full(h, p_full));
+            launch_mv<EPI_V>(h, false, p_full, V, &launched);  // v = M p, q.v -> a
             launch_seqdot<SQ_V>(h, V, &launched);
+            if (sh) TRY(exchange_point<FIN_V>(h, nullptr, &launched));
             launch_phase<PH_C>(h, V, &launched);               // s = r - a v, max|s|
-            launch_mv<EPI_T>(h, false, V.s, V, &launched);     // t = M s, t.t, t.s -> w
+            if (sh) TRY(allgather_full(h, s_full));
+            launch_mv<EPI_T>(h, false, s_full, V, &launched);  // t = M s, t.t, t.s -> w
             launch_seqdot<SQ_T>(h, V, &launched);
+            if (sh) TRY(exchange_point<FIN_T>(h, nullptr, &launched));
             launch_phase<PH_E>(h, V, &launched);               // x, r updates, q.r -> beta
             launch_seqdot<SQ_E>(h, V, &launched);
+            if (sh) TRY(exchange_point<FIN_E>(h, nullptr, &launched));
         }
         CK(cudaGetLastError());
         iters += k;
         TRY(read_state(h));
         batch = next_batch(batch);
     }
-    TRY(residual_into_state(h, V.x, &launched));
+    if (sh) TRY(allgather_full(h, h->vec(V_X)));  // this rank's x is its slice of V_X
+    TRY(residual_into_state(h, h->vec(V_X), &launched));
     CK(cudaEventRecord(h->ev1, h->stream));
     TRY(read_state(h));
     float ms = 0.f;
@@ -500,7 +612,7 @@ int host_solve(mcr_matrix* h, const double* b, const double* x0, double tol, int
     int rc = impl(h, db, x0 ? dx : nullptr, tol, max_it, dout, rep);
     if (rc == MCR_OK || rc == MCR_NOT_CONVERGED || rc == MCR_BREAKDOWN) {
         const double* src = dout;
-        if (rc == MCR_BREAKDOWN) src = h->vec(V_X);  // snapshot: x before that iteration
+        if (rc == MCR_BREAKDOWN) src = h->vec(V_X) + h->roff;  // snapshot: x before that iteration
         CK(cudaMemcpyAsync(x_out, src, bytes, cudaMemcpyDeviceToHost, h->stream));
         CK(cudaStreamSynchronize(h->stream));
     }
@@ -538,7 +650,7 @@ MCR_API void mcr_matrix_destroy(mcr_matrix* h) {
                             h->rrp, h->rcol, h->rval, h->dense, h->d, h->work, h->P, h->st,
                             h->sell.sptr, h->sell.perm, h->sell.col, h->sell.val, h->sell.swidth,
                             h->rsell.sptr, h->rsell.perm, h->rsell.col, h->rsell.val,
-                            h->rsell.swidth, h->maxslot};
+                            h->rsell.swidth, h->maxslot, h->recv};
             for (void* p : ptrs)
                 if (p) cudaFreeAsync(p, s);
             cudaStreamSynchronize(s);
@@ -561,6 +673,8 @@ static int set_kernel_attributes() {
     return MCR_OK;
 }
 
+// Rows [h->roff, h->roff + n) of an h->n_global system (the whole system on one GPU);
+// column indices are global.
 static int create_impl(mcr_matrix* h, int64_t n, const int64_t* rs, const int64_t* col,
                        const double* val, int storage) {
     TRY(keep_pool_memory(h->device));
@@ -573,9 +687,10 @@ static int create_impl(mcr_matrix* h, int64_t n, const int64_t* rs, const int64_
     if (n == 0) return MCR_OK;
     const int64_t nnz = rs[n];
     h->nnz = nnz;
-    const bool dense = storage == MCR_STORAGE_DENSE ||
-                       (storage == MCR_STORAGE_AUTO && n >= 1024 &&
-                        (double)nnz * 3.0 >= 2.0 * (double)n * (double)n);
+    const bool dense = !h->sharded() &&
+                       (storage == MCR_STORAGE_DENSE ||
+                        (storage == MCR_STORAGE_AUTO && n >= 1024 &&
+                         (double)nnz * 3.0 >= 2.0 * (double)n * (double)n));
     h->storage = dense ? MCR_STORAGE_DENSE : MCR_STORAGE_CSR;
 
     TRY(dalloc(h, &h->rp, (size_t)n + 1 + CSR_PAD));
@@ -599,7 +714,7 @@ static int create_impl(mcr_matrix* h, int64_t n, const int64_t* rs, const int64_
                            h->stream));
         if (nnz > 0)
             k_col64to32<<<(int)std::min<int64_t>((nnz + 255) / 256, 1 << 16), 256, 0, h->stream>>>(
-                tmp, h->col, nnz, (int)n, bad);
+                tmp, h->col, nnz, (int)h->n_global, bad);
         CK(cudaGetLastError());
         int hbad = 0;
         CK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
@@ -615,13 +730,13 @@ static int create_impl(mcr_matrix* h, int64_t n, const int64_t* rs, const int64_
         CK(cudaMemsetAsync(fz, 0xff, sizeof(unsigned long long), h->stream));
         CK(cudaMemsetAsync(h->offlen + n, 0, sizeof(long long), h->stream));
         k_diag<<<(int)std::min<int64_t>((n + 255) / 256, 1 << 16), 256, 0, h->stream>>>(
-            h->rp, h->col, h->val, (int)n, h->d, h->offlen, fz);
+            h->rp, h->col, h->val, (int)n, (long long)h->roff, h->d, h->offlen, fz);
         CK(cudaGetLastError());
         unsigned long long hfz = 0;
         CK(cudaMemcpyAsync(&hfz, fz, sizeof(hfz), cudaMemcpyDeviceToHost, h->stream));
         CK(cudaFreeAsync(fz, h->stream));
         CK(cudaStreamSynchronize(h->stream));
-        h->first_zero = hfz == ~0ull ? -1 : (long long)hfz;
+        h->first_zero = hfz == ~0ull ? -1 : (long long)hfz + h->roff;  // global row
     }
     std::vector<int> tiles = make_tiles(n, rs, &h->max_row);
     if (dense) {
@@ -646,7 +761,7 @@ static int create_impl(mcr_matrix* h, int64_t n, const int64_t* rs, const int64_
         // SELL streams rows without shared-memory staging, but its epilogue operands are
         // gathered through the row permutation; measured on C2 (profiles/) the TMA-staged
         // tiles win (54 vs 70 us per Jacobi sweep), so SELL is opt-in.
-        h->use_sell = storage == MCR_STORAGE_SELL;
+        h->use_sell = storage == MCR_STORAGE_SELL && !h->sharded();
         if (h->use_sell) TRY(build_sell(h, false, &h->sell));
         TRY(set_kernel_attributes());
         int sms = 0, per_sm = 0;
@@ -658,8 +773,8 @@ static int create_impl(mcr_matrix* h, int64_t n, const int64_t* rs, const int64_
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pb, k_bicg_small, SM_NT, 0));
         const int coresident = sms * std::min(pj, pb);
         // one tile per CTA keeps the per-sweep critical path to a single tile
-        if (!h->use_sell && storage != MCR_STORAGE_TILES_STREAM && h->ntiles <= coresident &&
-            h->ntiles <= 2 * sms)
+        if (!h->use_sell && !h->sharded() && storage != MCR_STORAGE_TILES_STREAM &&
+            h->ntiles <= coresident && h->ntiles <= 2 * sms)
             h->small_grid = h->ntiles;
         TRY(dalloc(h, &h->maxslot, 3));
         TRY(dalloc(h, &h->tile_row, tiles.size()));
@@ -677,10 +792,7 @@ static int create_impl(mcr_matrix* h, int64_t n, const int64_t* rs, const int64_
     return MCR_OK;
 }
 
-MCR_API int mcr_matrix_create(int64_t n, const int64_t* rstart, const int64_t* col,
-                              const double* nonzero, int device, int storage, mcr_matrix** out) {
-    if (!out) return fail(MCR_INVALID_ARGUMENT, "out is NULL");
-    *out = nullptr;
+static int check_csr(int64_t n, const int64_t* rstart, const int64_t* col, const double* nonzero) {
     if (n < 0 || n >= INT_MAX) return fail(MCR_DIMENSION, "dimension out of range");
     if (n > 0 && (!rstart || (rstart[n] > 0 && (!col || !nonzero))))
         return fail(MCR_INVALID_ARGUMENT, "NULL CSR array");
@@ -689,6 +801,13 @@ MCR_API int mcr_matrix_create(int64_t n, const int64_t* rstart, const int64_t* c
         for (int64_t i = 0; i < n; ++i)
             if (rstart[i + 1] < rstart[i]) return fail(MCR_DIMENSION, "rstart must be nondecreasing");
     }
+    return MCR_OK;
+}
+
+static int create_handle(int64_t n, const int64_t* rstart, const int64_t* col,
+                         const double* nonzero, int device, int storage,
+                         const std::shared_ptr<Transport>& comm, int64_t n_global, int64_t roff,
+                         int64_t chunk, mcr_matrix** out) {
     int ndev = 0;
     mcr_device_count(&ndev);
     if (device < 0 || device >= ndev)
@@ -698,6 +817,14 @@ MCR_API int mcr_matrix_create(int64_t n, const int64_t* rstart, const int64_t* c
     mcr_matrix* h = new mcr_matrix();
     h->device = device;
     h->n = n;
+    h->n_global = n_global;
+    h->roff = roff;
+    h->chunk = chunk;
+    if (comm) {
+        h->comm = comm;
+        h->world = comm->world;
+        h->rank = comm->rank;
+    }
     int rc = create_impl(h, n, rstart, col, nonzero, storage);
     if (rc != MCR_OK) {
         std::string msg = g_err;
@@ -707,6 +834,122 @@ MCR_API int mcr_matrix_create(int64_t n, const int64_t* rstart, const int64_t* c
     }
     *out = h;
     return MCR_OK;
+}
+
+MCR_API int mcr_matrix_create(int64_t n, const int64_t* rstart, const int64_t* col,
+                              const double* nonzero, int device, int storage, mcr_matrix** out) {
+    if (!out) return fail(MCR_INVALID_ARGUMENT, "out is NULL");
+    *out = nullptr;
+    TRY(check_csr(n, rstart, col, nonzero));
+    return create_handle(n, rstart, col, nonzero, device, storage, nullptr, n, 0, n, out);
+}
+
+// ---------------------------------------------------------------- row sharding
+MCR_API int mcr_shard_rows(int64_t n_global, int world, int rank, int64_t* row0, int64_t* rows) {
+    if (world < 1 || rank < 0 || rank >= world || n_global < 0 || !row0 || !rows)
+        return fail(MCR_INVALID_ARGUMENT, "bad shard request");
+    const int64_t chunk = (n_global + world - 1) / world;
+    const int64_t lo = std::min<int64_t>(n_global, chunk * rank);
+    const int64_t hi = std::min<int64_t>(n_global, lo + chunk);
+    *row0 = lo;
+    *rows = hi - lo;
+    return MCR_OK;
+}
+
+MCR_API int mcr_comm_unique_id(void* id) {
+    if (!id) return fail(MCR_INVALID_ARGUMENT, "NULL id");
+    NcclApi* api = NcclApi::get();
+    if (!api) return fail(MCR_CUDA_ERROR, NcclApi::error());
+    ncclUniqueId u;
+    ncclResult_t r = api->GetUniqueId(&u);
+    if (r != ncclSuccess) return fail(MCR_CUDA_ERROR, std::string("ncclGetUniqueId: ") + api->GetErrorString(r));
+    std::memcpy(id, &u, sizeof(u));
+    return MCR_OK;
+}
+
+MCR_API int mcr_comm_create_nccl(const void* id, int world, int rank, int device, mcr_comm** out) {
+    if (!id || !out) return fail(MCR_INVALID_ARGUMENT, "NULL argument");
+    *out = nullptr;
+    if (world < 1 || rank < 0 || rank >= world) return fail(MCR_INVALID_ARGUMENT, "bad rank / world");
+    NcclApi* api = NcclApi::get();
+    if (!api) return fail(MCR_CUDA_ERROR, NcclApi::error());
+    int ndev = 0;
+    mcr_device_count(&ndev);
+    if (device < 0 || device >= ndev) return fail(MCR_CUDA_ERROR, "no CUDA device " + std::to_string(device));
+    DeviceGuard g(device);
+    auto t = std::make_shared<NcclTransport>();
+    t->api = api;
+    t->world = world;
+    t->rank = rank;
+    t->device = device;
+    ncclUniqueId u;
+    std::memcpy(&u, id, sizeof(u));
+    ncclResult_t r = api->CommInitRank(&t->comm, world, u, rank);
+    if (r != ncclSuccess) {
+        t->comm = nullptr;
+        return fail(MCR_CUDA_ERROR, std::string("ncclCommInitRank: ") + api->GetErrorString(r));
+    }
+    *out = new mcr_comm{t};
+    return MCR_OK;
+}
+
+MCR_API int mcr_comm_create_local(int world, const int* devices, mcr_comm** out) {
+    if (!out || world < 1) return fail(MCR_INVALID_ARGUMENT, "bad local group request");
+    int ndev = 0;
+    mcr_device_count(&ndev);
+    auto g = std::make_shared<LocalGroup>();
+    g->world = world;
+    g->src.assign((size_t)world, nullptr);
+    g->dev.assign((size_t)world, 0);
+    g->ready.assign((size_t)world, nullptr);
+    g->done.assign((size_t)world, nullptr);
+    for (int r = 0; r < world; ++r) {
+        const int d = devices ? devices[r] : 0;
+        if (d < 0 || d >= ndev) return fail(MCR_CUDA_ERROR, "no CUDA device " + std::to_string(d));
+        g->dev[(size_t)r] = d;
+        DeviceGuard guard(d);
+        CK(cudaEventCreateWithFlags(&g->ready[(size_t)r], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&g->done[(size_t)r], cudaEventDisableTiming));
+    }
+    for (int r = 0; r < world; ++r) {
+        auto t = std::make_shared<LocalTransport>();
+        t->g = g;
+        t->world = world;
+        t->rank = r;
+        t->device = g->dev[(size_t)r];
+        out[r] = new mcr_comm{t};
+    }
+    return MCR_OK;
+}
+
+MCR_API void mcr_comm_destroy(mcr_comm* c) { delete c; }
+
+MCR_API int mcr_comm_info(const mcr_comm* c, int* world, int* rank, int* device) {
+    if (!c) return fail(MCR_INVALID_ARGUMENT, "NULL comm");
+    if (world) *world = c->t->world;
+    if (rank) *rank = c->t->rank;
+    if (device) *device = c->t->device;
+    return MCR_OK;
+}
+
+MCR_API int mcr_shard_create(mcr_comm* comm, int64_t n_global, int64_t row0, int64_t rows,
+                             const int64_t* rstart, const int64_t* col, const double* nonzero,
+                             mcr_matrix** out) {
+    if (!comm || !out) return fail(MCR_INVALID_ARGUMENT, "NULL argument");
+    *out = nullptr;
+    if (n_global < 0 || n_global >= INT_MAX) return fail(MCR_DIMENSION, "dimension out of range");
+    const Transport& T = *comm->t;
+    int64_t want0 = 0, want = 0;
+    TRY(mcr_shard_rows(n_global, T.world, T.rank, &want0, &want));
+    if (row0 != want0 || rows != want)
+        return fail(MCR_DIMENSION, "rank " + std::to_string(T.rank) + " of " + std::to_string(T.world) +
+                                       " must hold rows [" + std::to_string(want0) + ", " +
+                                       std::to_string(want0 + want) + ")");
+    if (rows < 1) return fail(MCR_DIMENSION, "every rank needs at least one row (n >= world)");
+    TRY(check_csr(rows, rstart, col, nonzero));
+    const int64_t chunk = (n_global + T.world - 1) / T.world;
+    return create_handle(rows, rstart, col, nonzero, T.device, MCR_STORAGE_TILES_STREAM, comm->t,
+                         n_global, row0, chunk, out);
 }
 
 MCR_API int mcr_matrix_info_get(const mcr_matrix* h, mcr_matrix_info* info) {
@@ -720,6 +963,10 @@ MCR_API int mcr_matrix_info_get(const mcr_matrix* h, mcr_matrix_info* info) {
     info->max_row_nnz = h->max_row;
     info->first_zero_diagonal = h->first_zero;
     info->device_bytes = h->bytes;
+    info->n_global = h->n_global;
+    info->row0 = h->roff;
+    info->world = h->world;
+    info->rank = h->rank;
     return MCR_OK;
 }
 
@@ -728,6 +975,8 @@ MCR_API int mcr_set_dot_mode(mcr_matrix* h, int mode) {
     if (mode != MCR_DOTS_TREE && mode != MCR_DOTS_SEQUENTIAL)
         return fail(MCR_INVALID_ARGUMENT, "unknown dot mode");
     std::lock_guard<std::mutex> lk(h->mu);
+    if (mode == MCR_DOTS_SEQUENTIAL && h->sharded())
+        return fail(MCR_INVALID_ARGUMENT, "sequential dots need the whole system on one GPU");
     h->seqdots = mode == MCR_DOTS_SEQUENTIAL;
     return MCR_OK;
 }
@@ -754,6 +1003,7 @@ MCR_API int mcr_matvec_device(mcr_matrix* h, const double* d_x, double* d_y) {
 
 MCR_API int mcr_matvec(mcr_matrix* h, const double* x, double* y) {
     if (!h) return fail(MCR_INVALID_ARGUMENT, "NULL handle");
+    if (h->sharded()) return fail(MCR_INVALID_ARGUMENT, "mcr_matvec: use mcr_matvec_device on a row shard");
     std::lock_guard<std::mutex> lk(h->mu);
     if (h->n == 0) return MCR_OK;
     DeviceGuard g(h->device);
@@ -772,6 +1022,7 @@ MCR_API int mcr_matvec(mcr_matrix* h, const double* x, double* y) {
 
 MCR_API int mcr_residual_inf(mcr_matrix* h, const double* x, const double* b, double* out) {
     if (!h || !out) return fail(MCR_INVALID_ARGUMENT, "NULL argument");
+    if (h->sharded()) return fail(MCR_INVALID_ARGUMENT, "mcr_residual_inf needs the whole system");
     std::lock_guard<std::mutex> lk(h->mu);
     *out = 0.0;
     if (h->n == 0) return MCR_OK;
@@ -816,10 +1067,6 @@ MCR_API int mcr_bicgstab_device(mcr_matrix* h, const double* d_b, const double* 
 MCR_API int mcr_jacobi(mcr_matrix* h, const double* b, const double* x0, double tol,
                        int64_t max_it, double* x_out, mcr_report* rep) {
     SOLVE_PROLOGUE
-    if (h->first_zero >= 0) {
-        rep->zero_diagonal_index = h->first_zero;
-        return fail(MCR_ZERO_DIAGONAL, "zero diagonal entry in row " + std::to_string(h->first_zero));
-    }
     return host_solve(h, b, x0, tol, max_it, x_out, rep, jacobi_impl);
 }
 

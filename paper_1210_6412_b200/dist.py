@@ -1,0 +1,264 @@
+"""Row-sharded solves over several GPUs.
+
+The reference parallelises one solve over CPU worker threads by contiguous row blocks
+(``_row_blocks``, ``mcreach/solvers.py:159-168``; ``jacobi_solve_parallel`` :233-274;
+``_ParOps`` :314-396): every worker computes its rows of ``x'`` (or of ``M p``) against the
+whole current vector, then a barrier. Here the workers are GPUs: rank ``r`` of ``world`` owns
+rows ``[r*c, min(n, (r+1)*c))`` with ``c = ceil(n / world)`` as a CSR whose columns stay
+global, and the barrier is an in-place allgather of the vector the next SpMV gathers from,
+plus an exchange of every rank's reduction partials (dots, max) that each rank then reduces
+in rank order -- so all ranks hold bit-identical scalars and take the same stop decision.
+Jacobi iterates are bit-identical to one GPU and to the reference at every world size
+(max is order-free), exactly as ``jacobi_solve_parallel`` is bit-identical to
+``jacobi_solve`` (``T/test_solvers.py:157-172``).
+
+Two transports behind the same C ABI (``include/mcr.h``):
+
+* ``Comm.nccl(device)`` -- one process per GPU (torchrun), NCCL over NVLink; the NCCL
+  unique id is broadcast with ``torch.distributed`` (any backend).
+* ``Comm.local_group(world)`` -- ``world`` ranks as threads of this process (on one or
+  several devices), collectives as event-ordered peer copies; ``solve_local_group`` uses it
+  to run the multi-rank path end to end on a single GPU.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+import time
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from .solvers import SolverConfig, SolveResult, _raise_native, outcome
+from .sparse import DimensionMismatch
+
+__all__ = ["shard_rows", "shard_of", "Comm", "ShardMatrix", "jacobi_solve_sharded",
+           "bicgstab_solve_sharded", "solve_local_group"]
+
+
+def shard_rows(n: int, world: int, rank: int):
+    """(first row, row count) of ``rank`` -- the same split as ``mcr_shard_rows``."""
+    if world < 1 or not 0 <= rank < world or n < 0:
+        raise ValueError(f"bad shard request n={n} world={world} rank={rank}")
+    c = -(-n // world)
+    lo = min(n, c * rank)
+    hi = min(n, lo + c)
+    return lo, hi - lo
+
+
+def shard_of(m, world: int, rank: int):
+    """This rank's rows of a CSR matrix: (row0, rows, local rstart, global col, nonzero)."""
+    row0, rows = shard_rows(int(m.n), world, rank)
+    rs = np.asarray(m.rstart, dtype=np.int64)[row0:row0 + rows + 1]
+    e0, e1 = int(rs[0]), int(rs[-1])
+    return (row0, rows, np.ascontiguousarray(rs - e0),
+            np.ascontiguousarray(np.asarray(m.col, dtype=np.int64)[e0:e1]),
+            np.ascontiguousarray(np.asarray(m.nonzero, dtype=np.float64)[e0:e1]))
+
+
+class Comm:
+    """A communicator handle (``mcr_comm``)."""
+
+    def __init__(self, handle: ctypes.c_void_p):
+        self._L = _lib.load()
+        self._h = handle
+        w, r, d = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        self._L.mcr_comm_info(handle, ctypes.byref(w), ctypes.byref(r), ctypes.byref(d))
+        self.world, self.rank, self.device = w.value, r.value, d.value
+
+    @property
+    def handle(self):
+        return self._h
+
+    @staticmethod
+    def unique_id() -> bytes:
+        L = _lib.load()
+        buf = ctypes.create_string_buffer(_lib.COMM_ID_BYTES)
+        rc = L.mcr_comm_unique_id(buf)
+        if rc != _lib.MCR_OK:
+            _raise_native(rc)
+        return buf.raw
+
+    @staticmethod
+    def broadcast_id(group=None) -> bytes:
+        """Rank 0 creates the NCCL id; every rank of the torch.distributed group receives it."""
+        import torch.distributed as dist
+        obj = [Comm.unique_id() if dist.get_rank(group) == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        return obj[0]
+
+    @classmethod
+    def nccl(cls, device: int, group=None, uid: Optional[bytes] = None) -> "Comm":
+        """Collective over the ranks of the (initialised) torch.distributed group."""
+        import torch.distributed as dist
+        if uid is None:
+            uid = cls.broadcast_id(group)
+        L = _lib.load()
+        h = ctypes.c_void_p()
+        rc = L.mcr_comm_create_nccl(uid, dist.get_world_size(group), dist.get_rank(group),
+                                    int(device), ctypes.byref(h))
+        if rc != _lib.MCR_OK:
+            _raise_native(rc)
+        return cls(h)
+
+    @classmethod
+    def local_group(cls, world: int, devices: Optional[Sequence[int]] = None) -> List["Comm"]:
+        L = _lib.load()
+        out = (ctypes.c_void_p * world)()
+        devs = None
+        if devices is not None:
+            devs = (ctypes.c_int * world)(*[int(d) for d in devices])
+        rc = L.mcr_comm_create_local(int(world), devs, out)
+        if rc != _lib.MCR_OK:
+            _raise_native(rc)
+        return [cls(ctypes.c_void_p(out[r])) for r in range(world)]
+
+    def close(self):
+        if self._h:
+            self._L.mcr_comm_destroy(self._h)
+            self._h = None
+
+
+class ShardMatrix:
+    """This rank's rows of an ``n_global`` system, resident on the communicator's device."""
+
+    def __init__(self, comm: Comm, n_global: int, row0: int, rows: int, rstart, col, nonzero):
+        L = _lib.load()
+        self._L = L
+        self.comm = comm
+        self.n_global, self.row0, self.n = int(n_global), int(row0), int(rows)
+        rs = np.ascontiguousarray(rstart, dtype=np.int64)
+        c = np.ascontiguousarray(col, dtype=np.int64)
+        v = np.ascontiguousarray(nonzero, dtype=np.float64)
+        h = ctypes.c_void_p()
+        rc = L.mcr_shard_create(comm.handle, self.n_global, self.row0, self.n, rs.ctypes.data,
+                                c.ctypes.data, v.ctypes.data, ctypes.byref(h))
+        if rc != _lib.MCR_OK:
+            _raise_native(rc)
+        self._h = h
+
+    @classmethod
+    def from_matrix(cls, comm: Comm, m) -> "ShardMatrix":
+        row0, rows, rs, col, val = shard_of(m, comm.world, comm.rank)
+        return cls(comm, int(m.n), row0, rows, rs, col, val)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def info(self) -> dict:
+        inf = _lib.MatrixInfo()
+        self._L.mcr_matrix_info_get(self._h, ctypes.byref(inf))
+        return {f: getattr(inf, f) for f, _ in _lib.MatrixInfo._fields_}
+
+    def close(self):
+        if self._h:
+            self._L.mcr_matrix_destroy(self._h)
+            self._h = None
+
+    def solve(self, method: str, b_local, x0_local, tol: float, max_it: int):
+        fn = {"jacobi": self._L.mcr_jacobi, "bicgstab": self._L.mcr_bicgstab}[method]
+        b = np.ascontiguousarray(b_local, dtype=np.float64)
+        if b.shape != (self.n,):
+            raise DimensionMismatch(f"right-hand side slice of shape {b.shape} for {self.n} rows")
+        x = np.empty(self.n)
+        x0p = None
+        if x0_local is not None:
+            x0 = np.ascontiguousarray(x0_local, dtype=np.float64)
+            x0p = x0.ctypes.data
+        rep = _lib.Report()
+        rc = fn(self._h, b.ctypes.data, x0p, float(tol), int(max_it), x.ctypes.data,
+                ctypes.byref(rep))
+        return rc, x, rep
+
+
+def _guess_slice(shard: ShardMatrix, cfg) -> Optional[np.ndarray]:
+    """solvers.py:153-156 on the whole vector, then this rank's rows."""
+    seed = getattr(cfg, "guess_seed", None)
+    if seed is None:
+        return None
+    return np.random.default_rng(seed).random(shard.n_global)[shard.row0:shard.row0 + shard.n]
+
+
+def _solve_sharded(method, shard: ShardMatrix, b_local, config, raise_errors=True):
+    cfg = config or SolverConfig()
+    start = time.perf_counter()
+    rc, x, rep = shard.solve(method, b_local, _guess_slice(shard, cfg), cfg.tolerance,
+                             cfg.max_iterations)
+    result, err = outcome(rc, x, rep, start)
+    if err is not None and raise_errors:
+        raise err
+    return result, err
+
+
+def jacobi_solve_sharded(shard: ShardMatrix, b_local, config: Optional[SolverConfig] = None):
+    """``jacobi_solve`` on this rank's rows; x of the result is this rank's slice."""
+    return _solve_sharded("jacobi", shard, b_local, config)[0]
+
+
+def bicgstab_solve_sharded(shard: ShardMatrix, b_local, config: Optional[SolverConfig] = None):
+    """``bicgstab_solve`` on this rank's rows; x of the result is this rank's slice."""
+    return _solve_sharded("bicgstab", shard, b_local, config)[0]
+
+
+def solve_local_group(method: str, m, b, world: int, config: Optional[SolverConfig] = None,
+                      devices: Optional[Sequence[int]] = None):
+    """Solve ``m x = b`` as ``world`` row shards driven by ``world`` threads of this process.
+
+    Returns ``(result, per_rank)``: the assembled SolveResult (full x, rank 0's iteration
+    count and residual) and every rank's own SolveResult. Raises the reference's exception
+    (with the assembled x) when the ranks report one.
+    """
+    b = np.asarray(b, dtype=np.float64)
+    if b.shape != (m.n,):
+        raise DimensionMismatch(f"right-hand side of shape {b.shape} against dimension {m.n}")
+    if m.n < 1 or shard_rows(int(m.n), world, world - 1)[1] < 1:
+        raise ValueError(f"{world} ranks need every rank to hold rows (n = {m.n})")
+    comms = Comm.local_group(world, devices)
+    shards = [None] * world
+    out = [None] * world
+    errs = [None] * world
+    start = time.perf_counter()
+
+    def run(r):
+        try:
+            sh = ShardMatrix.from_matrix(comms[r], m)
+            shards[r] = sh
+            out[r] = _solve_sharded(method, sh, b[sh.row0:sh.row0 + sh.n], config,
+                                    raise_errors=False)
+        except BaseException as e:  # surfaced below
+            errs[r] = e
+
+    try:
+        threads = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+    finally:
+        for sh in shards:
+            if sh is not None:
+                sh.close()
+        for c in comms:
+            c.close()
+    for e in errs:
+        if e is not None:
+            raise e
+    results = [o[0] for o in out]
+    kinds = [type(o[1]) for o in out]
+    if len(set(kinds)) != 1:
+        raise RuntimeError(f"ranks disagree on the outcome: {kinds}")
+    err0 = out[0][1]
+    if results[0] is None:  # ZeroDiagonal: no result
+        raise err0
+    x = np.concatenate([r.x for r in results])
+    full = SolveResult(x, results[0].iterations, results[0].converged, results[0].residual_inf,
+                       time.perf_counter() - start)
+    if err0 is not None:
+        from .solvers import Breakdown, NotConverged
+        if isinstance(err0, Breakdown):
+            raise Breakdown(err0.which, err0.iteration, full)
+        raise NotConverged(full)
+    return full, results

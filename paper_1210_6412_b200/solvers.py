@@ -245,18 +245,30 @@ def _solve(method: str, m, b, config, dots: Optional[str] = None) -> SolveResult
     with dm.lock:
         rc, x, rep = dm.solve(method, b, x0, cfg.tolerance, cfg.max_iterations,
                               dots or getattr(cfg, "dot_products", "tree"))
+    return finish(rc, x, rep, start)
+
+
+def outcome(rc: int, x: np.ndarray, rep, start: float):
+    """(SolveResult, exception or None) of a native solve; raises on library errors."""
     if rc == _lib.MCR_ZERO_DIAGONAL:
-        raise ZeroDiagonal(int(rep.zero_diagonal_index))
+        return None, ZeroDiagonal(int(rep.zero_diagonal_index))
     if rc not in (_lib.MCR_OK, _lib.MCR_NOT_CONVERGED, _lib.MCR_BREAKDOWN):
         _raise_native(rc)
-    iterations = int(rep.iterations)
-    result = SolveResult(x, iterations, rc == _lib.MCR_OK, float(rep.residual_inf),
+    result = SolveResult(x, int(rep.iterations), rc == _lib.MCR_OK, float(rep.residual_inf),
                          time.perf_counter() - start)
     if rc == _lib.MCR_BREAKDOWN:
-        raise Breakdown(_lib.BREAKDOWN_NAMES[int(rep.breakdown_which)],
-                        int(rep.breakdown_iteration), result)
+        return result, Breakdown(_lib.BREAKDOWN_NAMES[int(rep.breakdown_which)],
+                                 int(rep.breakdown_iteration), result)
     if rc == _lib.MCR_NOT_CONVERGED:
-        raise NotConverged(result)
+        return result, NotConverged(result)
+    return result, None
+
+
+def finish(rc: int, x: np.ndarray, rep, start: float) -> SolveResult:
+    """Map a native status onto the reference's result / exceptions (solvers.py:43-78)."""
+    result, err = outcome(rc, x, rep, start)
+    if err is not None:
+        raise err
     return result
 
 
