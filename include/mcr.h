@@ -172,6 +172,24 @@ MCR_API int mcr_shard_create(mcr_comm* comm, int64_t n_global, int64_t row0, int
                              const int64_t* rstart, const int64_t* col, const double* nonzero,
                              mcr_matrix** out);
 
+/* ---------------------------------------------------------------------------------------
+ * Synthetic systems built directly in HBM (config C5: n = 2e8 does not fit the reference's
+ * host generator). Family of generate_dd_matrix / generate_rhs (generator.py:100-132):
+ * strictly diagonally dominant, row i has k_i ~ Poisson(mean_offdiag) (capped at 64 and n-1)
+ * distinct off-diagonal columns uniform over the other n-1, values U{lo..hi}, diagonal =
+ * row sum + U{1..hi}; b_i ~ U{1..10}. Every row draws from its own counter-based stream keyed
+ * by (seed, global row), so the matrix is identical for any sharding. comm == NULL: the whole
+ * system on `device`; else this rank's rows on the communicator's device. The CPU oracle
+ * restates the generator bit for bit (orc_generate).
+ * ------------------------------------------------------------------------------------- */
+MCR_API int mcr_generate(mcr_comm* comm, int device, int64_t n_global, double mean_offdiag,
+                         int lo, int hi, uint64_t seed, int storage, mcr_matrix** out);
+/* This handle's rows of the right-hand side into device memory d_b. */
+MCR_API int mcr_generate_rhs(const mcr_matrix* m, uint64_t seed, double* d_b);
+/* Copy the handle's CSR back to host arrays (local rstart[n+1], global col[nnz] as int64,
+ * nonzero[nnz]); any pointer may be NULL. */
+MCR_API int mcr_matrix_export(mcr_matrix* m, int64_t* rstart, int64_t* col, double* nonzero);
+
 /* Message of the last failing call on this thread ("" if none). */
 MCR_API const char* mcr_last_error(void);
 

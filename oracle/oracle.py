@@ -50,6 +50,10 @@ def lib():
         L.orc_bicgstab.argtypes = [ctypes.c_int64, _i64p, _i64p, _f64p, _f64p, _f64p,
                                    ctypes.c_double, ctypes.c_int64, _i64p, _f64p,
                                    ctypes.POINTER(ctypes.c_int)]
+        L.orc_generate.argtypes = [ctypes.c_uint64, ctypes.c_int64, ctypes.c_double, ctypes.c_int,
+                                   ctypes.c_int, ctypes.c_int64, ctypes.c_int64, _i64p, _i64p,
+                                   _f64p]
+        L.orc_generate_rhs.argtypes = [ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64, _f64p]
         _lib = L
     return _lib
 
@@ -127,3 +131,35 @@ def bicgstab(m, b, tolerance=1e-10, max_iterations=10_000, guess_seed=None) -> d
                             ctypes.byref(which))
     return {"status": st, "x": x, "iterations": it.value, "converged": st == OK,
             "residual_inf": res.value, "which": BREAKDOWN_NAMES.get(which.value)}
+
+
+class _Rows:
+    """Row block of a generated system: n rows, local rstart, global col (int64), nonzero."""
+
+    def __init__(self, n, rstart, col, nonzero):
+        self.n, self.rstart, self.col, self.nonzero = n, rstart, col, nonzero
+
+    @property
+    def m(self):
+        return int(self.rstart[-1])
+
+
+def generate(seed: int, n: int, mean: float = 7.0, lo: int = 1, hi: int = 10, row0: int = 0,
+             rows=None):
+    """Rows [row0, row0 + rows) of the row-keyed synthetic system (csrc/generator.cuh)."""
+    rows = n - row0 if rows is None else rows
+    rs = np.zeros(rows + 1, dtype=np.int64)
+    L = lib()
+    L.orc_generate(seed, n, mean, lo, hi, row0, rows, _ptr(rs, _i64p), None, None)
+    col = np.empty(int(rs[-1]), dtype=np.int64)
+    val = np.empty(int(rs[-1]), dtype=np.float64)
+    L.orc_generate(seed, n, mean, lo, hi, row0, rows, _ptr(rs, _i64p), _ptr(col, _i64p),
+                   _ptr(val, _f64p))
+    return _Rows(rows, rs, col, val)
+
+
+def generate_rhs(seed: int, n: int, row0: int = 0, rows=None) -> np.ndarray:
+    rows = n - row0 if rows is None else rows
+    b = np.empty(rows)
+    lib().orc_generate_rhs(seed, row0, rows, _ptr(b, _f64p))
+    return b

@@ -29,7 +29,8 @@ EXPORTS = (
     "mcr_residual_inf", "mcr_jacobi", "mcr_jacobi_device", "mcr_bicgstab",
     "mcr_bicgstab_device", "mcr_last_error", "mcr_set_dot_mode",
     "mcr_shard_rows", "mcr_comm_unique_id", "mcr_comm_create_nccl", "mcr_comm_create_local",
-    "mcr_comm_destroy", "mcr_comm_info", "mcr_shard_create",
+    "mcr_comm_destroy", "mcr_comm_info", "mcr_shard_create", "mcr_generate",
+    "mcr_generate_rhs", "mcr_matrix_export",
 )
 COMM_ID_BYTES = 128
 DOTS_TREE, DOTS_SEQUENTIAL = 0, 1
@@ -112,6 +113,9 @@ def load():
     L.mcr_comm_destroy.restype = None
     L.mcr_comm_info.argtypes = [vp, pint, pint, pint]
     L.mcr_shard_create.argtypes = [vp, i64, i64, i64, vp, vp, vp, ctypes.POINTER(vp)]
+    L.mcr_generate.argtypes = [vp, ip, i64, dbl, ip, ip, ctypes.c_uint64, ip, ctypes.POINTER(vp)]
+    L.mcr_generate_rhs.argtypes = [vp, ctypes.c_uint64, vp]
+    L.mcr_matrix_export.argtypes = [vp, vp, vp, vp]
     L.mcr_last_error.restype = ctypes.c_char_p
     L.mcr_last_error.argtypes = []
     _lib = L

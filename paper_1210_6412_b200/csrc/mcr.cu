@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -22,6 +23,7 @@
 
 #include "comm.h"
 #include "device.cuh"
+#include "generator.cuh"
 #include "mcr.h"
 
 using namespace mcr;
@@ -675,8 +677,9 @@ static int set_kernel_attributes() {
 
 // Rows [h->roff, h->roff + n) of an h->n_global system (the whole system on one GPU);
 // column indices are global.
-static int create_impl(mcr_matrix* h, int64_t n, const int64_t* rs, const int64_t* col,
-                       const double* val, int storage) {
+static int finish_create(mcr_matrix* h, int64_t n, const int64_t* rs, int storage);
+
+static int init_handle(mcr_matrix* h) {
     TRY(keep_pool_memory(h->device));
     CK(cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking));
     h->stream = h->own_stream;
@@ -684,20 +687,25 @@ static int create_impl(mcr_matrix* h, int64_t n, const int64_t* rs, const int64_
     CK(cudaEventCreate(&h->ev1));
     TRY(dalloc(h, &h->st, 1));
     CK(cudaMemsetAsync(h->st, 0, sizeof(SolveState), h->stream));
-    if (n == 0) return MCR_OK;
-    const int64_t nnz = rs[n];
-    h->nnz = nnz;
-    const bool dense = !h->sharded() &&
-                       (storage == MCR_STORAGE_DENSE ||
-                        (storage == MCR_STORAGE_AUTO && n >= 1024 &&
-                         (double)nnz * 3.0 >= 2.0 * (double)n * (double)n));
-    h->storage = dense ? MCR_STORAGE_DENSE : MCR_STORAGE_CSR;
+    return MCR_OK;
+}
 
-    TRY(dalloc(h, &h->rp, (size_t)n + 1 + CSR_PAD));
+static int alloc_csr(mcr_matrix* h, int64_t n, int64_t nnz) {
+    h->nnz = nnz;
+    if (!h->rp) TRY(dalloc(h, &h->rp, (size_t)n + 1 + CSR_PAD));
     TRY(dalloc(h, &h->col, (size_t)nnz + CSR_PAD));
     TRY(dalloc(h, &h->val, (size_t)nnz + CSR_PAD));
     TRY(dalloc(h, &h->d, (size_t)n));
     TRY(dalloc(h, &h->offlen, (size_t)n + 1));
+    return MCR_OK;
+}
+
+static int create_impl(mcr_matrix* h, int64_t n, const int64_t* rs, const int64_t* col,
+                       const double* val, int storage) {
+    TRY(init_handle(h));
+    if (n == 0) return MCR_OK;
+    const int64_t nnz = rs[n];
+    TRY(alloc_csr(h, n, nnz));
     CK(cudaMemcpyAsync(h->rp, rs, sizeof(long long) * (size_t)(n + 1), cudaMemcpyHostToDevice,
                        h->stream));
     CK(cudaMemcpyAsync(h->val, val, sizeof(double) * (size_t)nnz, cudaMemcpyHostToDevice,
@@ -723,6 +731,59 @@ static int create_impl(mcr_matrix* h, int64_t n, const int64_t* rs, const int64_
         CK(cudaStreamSynchronize(h->stream));
         if (hbad) return fail(MCR_DIMENSION, "column index out of range");
     }
+    return finish_create(h, n, rs, storage);
+}
+
+// Poisson(mean) inverse-CDF thresholds on 2^64 (generator.cuh); restated in oracle.c.
+static void poisson_thresholds(double mean, uint64_t* thr) {
+    double p = std::exp(-mean), cdf = 0.0;
+    for (int k = 0; k < GEN_KMAX; ++k) {
+        cdf += p;
+        const double t = cdf * 18446744073709551616.0;
+        thr[k] = t >= 18446744073709551616.0 ? UINT64_MAX : (uint64_t)t;
+        p = (p * mean) / (double)(k + 1);
+    }
+}
+
+// Rows [h->roff, h->roff + h->n) of the row-keyed synthetic system, built on the device.
+static int generate_impl(mcr_matrix* h, const GenParams& P, int storage) {
+    TRY(init_handle(h));
+    const int64_t n = h->n;
+    if (n == 0) return MCR_OK;
+    TRY(dalloc(h, &h->rp, (size_t)n + 1 + CSR_PAD));
+    long long* len = nullptr;
+    CK(cudaMallocAsync((void**)&len, sizeof(long long) * (size_t)(n + 1), h->stream));
+    CK(cudaMemsetAsync(len + n, 0, sizeof(long long), h->stream));
+    const int grid = (int)std::min<int64_t>((n + 255) / 256, 1 << 16);
+    k_gen_count<<<grid, 256, 0, h->stream>>>(P, (long long)n, len);
+    CK(cudaGetLastError());
+    size_t tmp = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, len, h->rp, n + 1, h->stream));
+    void* dtmp = nullptr;
+    CK(cudaMallocAsync(&dtmp, tmp, h->stream));
+    CK(cub::DeviceScan::ExclusiveSum(dtmp, tmp, len, h->rp, n + 1, h->stream));
+    CK(cudaFreeAsync(dtmp, h->stream));
+    CK(cudaFreeAsync(len, h->stream));
+    std::vector<int64_t> rs((size_t)n + 1);
+    CK(cudaMemcpyAsync(rs.data(), h->rp, sizeof(int64_t) * rs.size(), cudaMemcpyDeviceToHost,
+                       h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    TRY(alloc_csr(h, n, rs[(size_t)n]));
+    k_gen_fill<<<(int)std::min<int64_t>((n + 127) / 128, 1 << 20), 128, 0, h->stream>>>(
+        P, (long long)n, h->rp, h->col, h->val);
+    CK(cudaGetLastError());
+    return finish_create(h, n, rs.data(), storage);
+}
+
+// Device CSR (rp/col/val) in place; `rs` = host copy of the row starts. Diagonal, tiles or
+// dense slabs, kernel attributes.
+static int finish_create(mcr_matrix* h, int64_t n, const int64_t* rs, int storage) {
+    const int64_t nnz = h->nnz;
+    const bool dense = !h->sharded() &&
+                       (storage == MCR_STORAGE_DENSE ||
+                        (storage == MCR_STORAGE_AUTO && n >= 1024 &&
+                         (double)nnz * 3.0 >= 2.0 * (double)n * (double)n));
+    h->storage = dense ? MCR_STORAGE_DENSE : MCR_STORAGE_CSR;
     // diagonal, first zero-diagonal row, off-diagonal row lengths
     {
         unsigned long long* fz = nullptr;
@@ -950,6 +1011,91 @@ MCR_API int mcr_shard_create(mcr_comm* comm, int64_t n_global, int64_t row0, int
     const int64_t chunk = (n_global + T.world - 1) / T.world;
     return create_handle(rows, rstart, col, nonzero, T.device, MCR_STORAGE_TILES_STREAM, comm->t,
                          n_global, row0, chunk, out);
+}
+
+MCR_API int mcr_generate(mcr_comm* comm, int device, int64_t n_global, double mean_offdiag,
+                         int lo, int hi, uint64_t seed, int storage, mcr_matrix** out) {
+    if (!out) return fail(MCR_INVALID_ARGUMENT, "out is NULL");
+    *out = nullptr;
+    if (n_global < 2 || n_global >= INT_MAX) return fail(MCR_DIMENSION, "need 2 <= n < 2^31");
+    if (!(mean_offdiag >= 0.0 && mean_offdiag <= 40.0) || lo > hi || hi < 1)
+        return fail(MCR_INVALID_ARGUMENT, "need 0 <= mean_offdiag <= 40 and 1 <= hi, lo <= hi");
+    int world = 1, rank = 0;
+    if (comm) {
+        world = comm->t->world;
+        rank = comm->t->rank;
+        device = comm->t->device;
+    }
+    int64_t row0 = 0, rows = n_global;
+    TRY(mcr_shard_rows(n_global, world, rank, &row0, &rows));
+    if (rows < 1) return fail(MCR_DIMENSION, "every rank needs at least one row (n >= world)");
+    int ndev = 0;
+    mcr_device_count(&ndev);
+    if (device < 0 || device >= ndev) return fail(MCR_CUDA_ERROR, "no CUDA device " + std::to_string(device));
+    DeviceGuard g(device);
+    mcr_matrix* h = new mcr_matrix();
+    h->device = device;
+    h->n = rows;
+    h->n_global = n_global;
+    h->roff = row0;
+    h->chunk = (n_global + world - 1) / world;
+    if (comm) {
+        h->comm = comm->t;
+        h->world = world;
+        h->rank = rank;
+        storage = MCR_STORAGE_TILES_STREAM;
+    }
+    GenParams P{};
+    P.seed = seed;
+    P.n = n_global;
+    P.row0 = row0;
+    P.lo = lo;
+    P.hi = hi;
+    poisson_thresholds(mean_offdiag, P.thr);
+    int rc = generate_impl(h, P, storage);
+    if (rc != MCR_OK) {
+        std::string msg = g_err;
+        mcr_matrix_destroy(h);
+        g_err = msg;
+        return rc;
+    }
+    *out = h;
+    return MCR_OK;
+}
+
+MCR_API int mcr_generate_rhs(const mcr_matrix* h, uint64_t seed, double* d_b) {
+    if (!h || !d_b) return fail(MCR_INVALID_ARGUMENT, "NULL argument");
+    if (h->n == 0) return MCR_OK;
+    DeviceGuard g(h->device);
+    k_gen_rhs<<<(int)std::min<int64_t>((h->n + 255) / 256, 1 << 16), 256, 0, h->stream>>>(
+        seed, (long long)h->roff, (long long)h->n, d_b);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(h->stream));
+    return MCR_OK;
+}
+
+MCR_API int mcr_matrix_export(mcr_matrix* h, int64_t* rstart, int64_t* col, double* nonzero) {
+    if (!h) return fail(MCR_INVALID_ARGUMENT, "NULL handle");
+    std::lock_guard<std::mutex> lk(h->mu);
+    if (h->n == 0) {
+        if (rstart) rstart[0] = 0;
+        return MCR_OK;
+    }
+    if (!h->col || !h->val) return fail(MCR_INVALID_ARGUMENT, "dense-storage handle keeps no CSR");
+    DeviceGuard g(h->device);
+    const size_t n = (size_t)h->n, nnz = (size_t)h->nnz;
+    if (rstart)
+        CK(cudaMemcpyAsync(rstart, h->rp, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost, h->stream));
+    if (nonzero)
+        CK(cudaMemcpyAsync(nonzero, h->val, sizeof(double) * nnz, cudaMemcpyDeviceToHost, h->stream));
+    if (col) {
+        std::vector<int> c32(nnz);
+        CK(cudaMemcpyAsync(c32.data(), h->col, sizeof(int) * nnz, cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        for (size_t k = 0; k < nnz; ++k) col[k] = c32[k];
+    }
+    CK(cudaStreamSynchronize(h->stream));
+    return MCR_OK;
 }
 
 MCR_API int mcr_matrix_info_get(const mcr_matrix* h, mcr_matrix_info* info) {

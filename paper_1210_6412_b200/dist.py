@@ -124,20 +124,52 @@ class Comm:
 class ShardMatrix:
     """This rank's rows of an ``n_global`` system, resident on the communicator's device."""
 
-    def __init__(self, comm: Comm, n_global: int, row0: int, rows: int, rstart, col, nonzero):
+    def __init__(self, comm: Comm, n_global: int, row0: int, rows: int, rstart, col, nonzero,
+                 _handle=None):
         L = _lib.load()
         self._L = L
         self.comm = comm
         self.n_global, self.row0, self.n = int(n_global), int(row0), int(rows)
-        rs = np.ascontiguousarray(rstart, dtype=np.int64)
-        c = np.ascontiguousarray(col, dtype=np.int64)
-        v = np.ascontiguousarray(nonzero, dtype=np.float64)
+        if _handle is None:
+            rs = np.ascontiguousarray(rstart, dtype=np.int64)
+            c = np.ascontiguousarray(col, dtype=np.int64)
+            v = np.ascontiguousarray(nonzero, dtype=np.float64)
+            h = ctypes.c_void_p()
+            rc = L.mcr_shard_create(comm.handle, self.n_global, self.row0, self.n,
+                                    rs.ctypes.data, c.ctypes.data, v.ctypes.data, ctypes.byref(h))
+            if rc != _lib.MCR_OK:
+                _raise_native(rc)
+            _handle = h
+        self._h = _handle
+
+    @classmethod
+    def generated(cls, comm: Comm, n: int, mean_offdiag: float = 7.0, lo: int = 1, hi: int = 10,
+                  seed: int = 0) -> "ShardMatrix":
+        """This rank's rows of the row-keyed synthetic system, generated in HBM (config C5)."""
+        L = _lib.load()
         h = ctypes.c_void_p()
-        rc = L.mcr_shard_create(comm.handle, self.n_global, self.row0, self.n, rs.ctypes.data,
-                                c.ctypes.data, v.ctypes.data, ctypes.byref(h))
+        rc = L.mcr_generate(comm.handle, comm.device, int(n), float(mean_offdiag), int(lo),
+                            int(hi), int(seed), _lib.STORAGE_TILES_STREAM, ctypes.byref(h))
         if rc != _lib.MCR_OK:
             _raise_native(rc)
-        self._h = h
+        row0, rows = shard_rows(int(n), comm.world, comm.rank)
+        return cls(comm, n, row0, rows, None, None, None, _handle=h)
+
+    def generated_rhs(self, seed: int, out_device_ptr: int) -> None:
+        rc = self._L.mcr_generate_rhs(self._h, int(seed), ctypes.c_void_p(out_device_ptr))
+        if rc != _lib.MCR_OK:
+            _raise_native(rc)
+
+    def solve_device(self, method: str, d_b: int, d_x0, tol: float, max_it: int, d_x: int):
+        """Device-pointer solve of this rank's rows (inputs resident in HBM)."""
+        fn = {"jacobi": self._L.mcr_jacobi_device, "bicgstab": self._L.mcr_bicgstab_device}[method]
+        rep = _lib.Report()
+        rc = fn(self._h, ctypes.c_void_p(d_b), None if d_x0 is None else ctypes.c_void_p(d_x0),
+                float(tol), int(max_it), ctypes.c_void_p(d_x), ctypes.byref(rep))
+        return rc, rep
+
+    def set_stream(self, stream_ptr: int) -> None:
+        self._L.mcr_set_stream(self._h, ctypes.c_void_p(stream_ptr))
 
     @classmethod
     def from_matrix(cls, comm: Comm, m) -> "ShardMatrix":

@@ -117,23 +117,58 @@ def _ptr(a: np.ndarray) -> int:
 class DeviceMatrix:
     """Device-resident copy of a CSR matrix (one libmcr handle)."""
 
-    def __init__(self, m, device: int = 0, storage: int = _lib.STORAGE_AUTO):
+    def __init__(self, m, device: int = 0, storage: int = _lib.STORAGE_AUTO, _handle=None):
         L = _lib.load()
-        n = int(m.n)
-        rs = np.ascontiguousarray(m.rstart, dtype=np.int64)
-        col = np.ascontiguousarray(m.col, dtype=np.int64)
-        val = np.ascontiguousarray(m.nonzero, dtype=np.float64)
-        h = ctypes.c_void_p()
-        rc = L.mcr_matrix_create(n, _ptr(rs), _ptr(col), _ptr(val), int(device), int(storage),
-                                 ctypes.byref(h))
-        if rc != _lib.MCR_OK:
-            _raise_native(rc)
+        if _handle is None:
+            n = int(m.n)
+            rs = np.ascontiguousarray(m.rstart, dtype=np.int64)
+            col = np.ascontiguousarray(m.col, dtype=np.int64)
+            val = np.ascontiguousarray(m.nonzero, dtype=np.float64)
+            h = ctypes.c_void_p()
+            rc = L.mcr_matrix_create(n, _ptr(rs), _ptr(col), _ptr(val), int(device),
+                                     int(storage), ctypes.byref(h))
+            if rc != _lib.MCR_OK:
+                _raise_native(rc)
+        else:
+            h = _handle
         self._h = h
         self._L = L
-        self.n = n
-        self.device = int(device)
         self.lock = threading.Lock()
         self._finalizer = weakref.finalize(self, L.mcr_matrix_destroy, h)
+        inf = self.info()
+        self.n = int(inf["n"])
+        self.device = int(inf["device"])
+
+    @classmethod
+    def generated(cls, n: int, mean_offdiag: float = 7.0, lo: int = 1, hi: int = 10,
+                  seed: int = 0, device: int = 0, storage: int = _lib.STORAGE_AUTO,
+                  comm=None) -> "DeviceMatrix":
+        """Row-keyed synthetic system built in HBM (mcr_generate; config C5). With ``comm``
+        (a dist.Comm) the handle holds that rank's rows only."""
+        L = _lib.load()
+        h = ctypes.c_void_p()
+        rc = L.mcr_generate(comm.handle if comm is not None else None, int(device), int(n),
+                            float(mean_offdiag), int(lo), int(hi), int(seed), int(storage),
+                            ctypes.byref(h))
+        if rc != _lib.MCR_OK:
+            _raise_native(rc)
+        return cls(None, _handle=h)
+
+    def generated_rhs(self, seed: int, out_device_ptr: int) -> None:
+        rc = self._L.mcr_generate_rhs(self._h, int(seed), ctypes.c_void_p(out_device_ptr))
+        if rc != _lib.MCR_OK:
+            _raise_native(rc)
+
+    def export(self):
+        """Host copy of the handle's CSR: (local rstart, global col, nonzero)."""
+        inf = self.info()
+        rs = np.empty(int(inf["n"]) + 1, dtype=np.int64)
+        col = np.empty(int(inf["nnz"]), dtype=np.int64)
+        val = np.empty(int(inf["nnz"]), dtype=np.float64)
+        rc = self._L.mcr_matrix_export(self._h, _ptr(rs), _ptr(col), _ptr(val))
+        if rc != _lib.MCR_OK:
+            _raise_native(rc)
+        return rs, col, val
 
     @property
     def handle(self) -> ctypes.c_void_p:

@@ -110,3 +110,48 @@ def test_oracle_dot_matches_scalar_loop():
         for a, c in zip(u.tolist(), v.tolist()):
             acc += a * c
         assert oracle.dot(u, v) == acc
+
+
+# ------------------------------------------------------------------ C5 row-keyed generator
+def test_generator_c5_family_properties():
+    """The oracle restatement of csrc/generator.cuh: strictly dominant, rows sorted, mean
+    row length 1 + mean_offdiag, values in range, diagonal present once per row."""
+    from oracle import oracle
+    n = 20000
+    g = oracle.generate(11, n, 7.0)
+    lens = np.diff(g.rstart)
+    assert abs(lens.mean() - 8.0) < 0.1 and lens.min() >= 1
+    rid = np.repeat(np.arange(n), lens)
+    assert np.all((np.diff(g.col) > 0) | (np.diff(rid) > 0))
+    on = g.col == rid
+    assert np.array_equal(np.bincount(rid[on], minlength=n), np.ones(n))
+    off = ~on
+    assert g.nonzero[off].min() >= 1 and g.nonzero[off].max() <= 10
+    sums = np.bincount(rid[off], weights=g.nonzero[off], minlength=n)
+    slack = g.nonzero[on] - sums
+    assert slack.min() >= 1 and slack.max() <= 10
+    b = oracle.generate_rhs(11, n)
+    assert b.min() >= 1 and b.max() <= 10 and np.all(b == np.round(b))
+
+
+def test_generator_c5_shard_invariant():
+    from oracle import oracle
+    from paper_1210_6412_b200 import dist
+    n = 5003
+    full = oracle.generate(3, n, 7.0)
+    for world in (2, 3, 8):
+        for r in range(world):
+            row0, rows = dist.shard_rows(n, world, r)
+            part = oracle.generate(3, n, 7.0, row0=row0, rows=rows)
+            e0, e1 = full.rstart[row0], full.rstart[row0 + rows]
+            assert np.array_equal(part.rstart, full.rstart[row0:row0 + rows + 1] - e0)
+            assert np.array_equal(part.col, full.col[e0:e1])
+            assert np.array_equal(part.nonzero, full.nonzero[e0:e1])
+            assert np.array_equal(oracle.generate_rhs(3, n, row0, rows),
+                                  oracle.generate_rhs(3, n)[row0:row0 + rows])
+
+
+def test_generator_c5_tiny_dimension_caps_count():
+    from oracle import oracle
+    g = oracle.generate(1, 3, 30.0)  # k capped at n - 1 = 2: dense 3x3
+    assert np.array_equal(np.diff(g.rstart), [3, 3, 3])
