@@ -81,13 +81,18 @@ def load_peak():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def load_traffic(kernel_key: str):
-    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
-    try:
-        with open(path) as fh:
-            return json.load(fh)["kernels"][kernel_key]["dram_bytes_per_launch"]
-    except Exception:
-        return None
+def load_traffic(kernel_key: str, prefix: str = "c2"):
+    """DRAM bytes per launch of `kernel_key` from the newest committed ncu summary
+    (profiles/rNN_<prefix>_ncu.json, one `ncu --set full` capture)."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_{prefix}_ncu.json")),
+                       reverse=True):
+        try:
+            with open(path) as fh:
+                return json.load(fh)["kernels"][kernel_key]["dram_bytes_per_launch"]
+        except Exception:
+            continue
+    return None
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -399,17 +404,201 @@ def run_ours(args):
     return 0
 
 
+# ----------------------------------------------------------------------------- C5 (sharded)
+
+def c5_cpu_proxy(threads: int, n_proxy: int, sweeps: int, n_full: int, iters: dict):
+    """The reference path cannot build C5 (n = 2e8; its generator needs ~141 B/nnz of host
+    RAM). Bounded sample: the oracle's Jacobi sweep (the reference's operation
+    order, all host threads) on an n_proxy-row system of the same family, `sweeps` sweeps,
+    scaled linearly to n_full rows and to the GPU run's iteration counts."""
+    from oracle import oracle
+    oracle.set_threads(threads)
+    m = oracle.generate(2024, n_proxy, 7.0)
+    b = oracle.generate_rhs(2024, n_proxy)
+    t0 = time.perf_counter()
+    oracle.jacobi(m, b, max_iterations=sweeps)
+    per_sweep = (time.perf_counter() - t0) / sweeps * (n_full / n_proxy)
+    # one BiCGStab iteration ~ 2 SpMV + vector work ~ 2.5 Jacobi sweeps (SURVEY 6 ratios)
+    pair = per_sweep * iters["jacobi"] + 2.5 * per_sweep * iters["bicgstab"]
+    return 2.0 / pair, (f"oracle Jacobi, {sweeps} sweeps on an n={n_proxy:.0e} system of the C5 "
+                        f"family ({threads} threads), per-sweep time scaled x{n_full / n_proxy:.0f} "
+                        f"to n={n_full:.0e} and to the GPU iteration counts "
+                        f"({iters['jacobi']} sweeps + {iters['bicgstab']} BiCGStab iterations "
+                        f"at 2.5 sweeps each): extrapolated, not run")
+
+
+def run_c5(args):
+    import ctypes
+
+    import torch
+
+    from paper_1210_6412_b200 import _lib
+    from paper_1210_6412_b200.dist import Comm, ShardMatrix
+    from paper_1210_6412_b200.solvers import DeviceMatrix
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    L = _lib.load()
+    n, mean, seed = args.n, 7.0, 2024
+    t_gen = time.perf_counter()
+    if world > 1:
+        comm = Comm.nccl(local)
+        h = ShardMatrix.generated(comm, n, mean, 1, 10, seed)
+    else:
+        comm = None
+        h = DeviceMatrix.generated(n, mean, 1, 10, seed, device=local, storage=_lib.STORAGE_TILES)
+    info = h.info()
+    rows, nnz_local = int(info["n"]), int(info["nnz"])
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    L.mcr_set_stream(h.handle, ctypes.c_void_p(stream.cuda_stream))
+    b = torch.empty(rows, dtype=torch.float64, device=dev)
+    h.generated_rhs(seed, b.data_ptr())
+    x = torch.empty(rows, dtype=torch.float64, device=dev)
+    torch.cuda.synchronize()
+    t_gen = time.perf_counter() - t_gen
+    nnz = torch.tensor([nnz_local], dtype=torch.int64, device=dev)
+    if dist:
+        dist.all_reduce(nnz)
+    nnz = int(nnz.item())
+
+    def solve(fn):
+        rep = _lib.Report()
+        rc = fn(h.handle, ctypes.c_void_p(b.data_ptr()), None, 1e-10, 10_000,
+                ctypes.c_void_p(x.data_ptr()), ctypes.byref(rep))
+        if rc not in (_lib.MCR_OK, _lib.MCR_NOT_CONVERGED):
+            raise RuntimeError(f"solve failed rc={rc}: {_lib.last_error()}")
+        return rep
+
+    def step():
+        return solve(L.mcr_jacobi_device), solve(L.mcr_bicgstab_device)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    step_ms, launches, reps = [], 0, None
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            rj, rb = step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+            launches += rj.kernel_launches + rb.kernel_launches
+            reps = (rj, rb)
+    total_ms = sum(step_ms)
+    if dist:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = 2.0 * args.steps / (total_ms / 1e3)   # solves of the ONE sharded system per second
+
+    # SpMV of this rank's rows against the full x (k_spmv<EPI_Y>), L2 is far smaller than x
+    xin = torch.rand(-(-n // world) * world, dtype=torch.float64, device=dev)
+    y = torch.empty(rows, dtype=torch.float64, device=dev)
+    sp = []
+    for i in range(3 + 5):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        L.mcr_matvec_device(h.handle, ctypes.c_void_p(xin.data_ptr()), ctypes.c_void_p(y.data_ptr()))
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if i >= 3:
+            sp.append(e0.elapsed_time(e1))
+    spmv_s = statistics.mean(sp) / 1e3
+    alg = 12 * nnz_local + 8 * (rows + 1) + 8 * rows + 8 * rows  # local rows; x read once per own row
+    peak, peak_src = load_peak()
+    achieved = alg / spmv_s / 1e9
+
+    # e2e through the public host-pointer C ABI: b from pinned host memory, x back to host
+    bh = torch.empty(rows, dtype=torch.float64).pin_memory()
+    bh.copy_(b.cpu())
+    xh = torch.empty(rows, dtype=torch.float64).pin_memory()
+    e2e = []
+    for i in range(1 + max(1, args.steps // 2)):
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for fn in (L.mcr_jacobi, L.mcr_bicgstab):
+            rep = _lib.Report()
+            rc = fn(h.handle, ctypes.c_void_p(bh.data_ptr()), None, 1e-10, 10_000,
+                    ctypes.c_void_p(xh.data_ptr()), ctypes.byref(rep))
+            assert rc in (_lib.MCR_OK, _lib.MCR_NOT_CONVERGED), _lib.last_error()
+        if i >= 1:
+            e2e.append(time.perf_counter() - t0)
+    e2e_total = sum(e2e)
+    if dist:
+        t = torch.tensor([e2e_total], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_total = float(t.item())
+    e2e_value = 2.0 * len(e2e) / e2e_total
+
+    rj, rb = reps
+    iters = {"jacobi": int(rj.iterations), "bicgstab": int(rb.iterations)}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        v, sample = c5_cpu_proxy(threads, 2 * 10 ** 6, 5, n, iters)
+        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: row-keyed device generator of the reference's DD family (C5)",
+        "config": {"workload": f"C5: n={n}, ~8 nnz/row (1 + Poisson(7)), row-sharded over {world} GPU(s)",
+                   "n": n, "nnz": nnz, "tolerance": 1e-10,
+                   "solve_pair": "jacobi + bicgstab (tree dots) from x0=0",
+                   "l2": "inputs (x 1.6 GB, matrix ~19 GB) far larger than L2",
+                   "parallelism": f"row shards x{world} (NCCL allgather + rank-order reductions)",
+                   "generation_s": t_gen},
+        "iterations": iters,
+        "time_to_solution_ms": {"jacobi": rj.device_seconds * 1e3, "bicgstab": rb.device_seconds * 1e3},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "kernel": "k_spmv<EPI_Y> on this rank's rows",
+                     "algorithmic_bytes": alg, "launch_us": spmv_s * 1e6, "peak_source": peak_src},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 2 * 8 * rows,
+                "d2h_bytes_per_step": 2 * 8 * rows,
+                "note": "mcr_jacobi + mcr_bicgstab with pinned host b / x; matrix generated in HBM"},
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+    }
+    if cpu:
+        line["cpu_baseline"] = cpu
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c5"])
+    ap.add_argument("--n", type=int, default=2 * 10 ** 8, help="C5 dimension")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
+    if args.config == "c5":
+        return run_c5(args)
     return run_ours(args)
 
 
