@@ -352,7 +352,7 @@ template <int EPI>
 void launch_mv(mcr_matrix* h, bool offdiag, const double* x, const Vecs& V, int64_t* launches) {
     if (h->storage == MCR_STORAGE_DENSE) {
         launch_pdl(k_dense<EPI>, h->nslabs, 32, DENSE_SMEM, h->stream, (const double*)h->dense,
-                   (int)h->n, x, V, h->st);
+                   (int)h->n, (int)((h->n + 1) & ~1ll), x, V, h->st);
     } else if (h->use_sell) {
         const auto& S = offdiag ? h->rsell : h->sell;
         launch_pdl(k_sell<EPI>, S.nwin * (SELL_W / SELL_CTA), SELL_CTA, 0, h->stream,
@@ -802,10 +802,12 @@ static int finish_create(mcr_matrix* h, int64_t n, const int64_t* rs, int storag
     std::vector<int> tiles = make_tiles(n, rs, &h->max_row);
     if (dense) {
         h->nslabs = (int)((n + DSLAB - 1) / DSLAB);
-        const size_t cnt = (size_t)h->nslabs * DSLAB * (size_t)n;
+        const int64_t npad = (n + 1) & ~1ll;  // column pairs
+        const size_t cnt = (size_t)h->nslabs * DSLAB * (size_t)npad;
         TRY(dalloc(h, &h->dense, cnt));
         CK(cudaMemsetAsync(h->dense, 0, sizeof(double) * cnt, h->stream));
-        k_dense_build<<<(int)n, 256, 0, h->stream>>>(h->rp, h->col, h->val, (int)n, h->dense);
+        k_dense_build<<<(int)n, 256, 0, h->stream>>>(h->rp, h->col, h->val, (int)n, (int)npad,
+                                                     h->dense);
         CK(cudaGetLastError());
         CK(cudaStreamSynchronize(h->stream));
         dfree(h, h->col, (size_t)nnz + CSR_PAD);
