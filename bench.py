@@ -316,8 +316,13 @@ def run_ours(args):
             spmv_ms.append(e0.elapsed_time(e1))
     spmv_s = statistics.mean(spmv_ms) / 1e3
     peak, peak_src = load_peak()
+    dense = dm.info()["storage"] == _lib.STORAGE_DENSE
+    if dense:  # dense GEMV 8n^2 + 16n, Jacobi 8n^2 + 32n, BiCGStab 16n^2 + 152n
+        ab = {"spmv": 8 * n * n + 16 * n, "jacobi_sweep": 8 * n * n + 32 * n,
+              "bicgstab_iteration": 16 * n * n + 152 * n}
+    kernel = "k_dense<EPI_Y>" if dense else "k_spmv<EPI_Y>"
     achieved = ab["spmv"] / spmv_s / 1e9
-    traffic = load_traffic("k_spmv<EPI_Y>")
+    traffic = load_traffic(kernel, {"c2": "c2", "c3": "c3dense"}.get(args.config, "none"))
 
     # ---- end to end through the public API with pinned host buffers
     def pinned(a):
@@ -386,7 +391,7 @@ def run_ours(args):
         },
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "k_spmv<EPI_Y> (CSR SpMV, one launch = one full M x)",
+                     "kernel": kernel + " (one launch = one full M x)",
                      "algorithmic_bytes": ab["spmv"], "launch_us": spmv_s * 1e6,
                      "peak_source": peak_src},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,

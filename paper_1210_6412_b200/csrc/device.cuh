@@ -130,6 +130,23 @@ __device__ __forceinline__ unsigned long long umax(unsigned long long a, unsigne
     return a > b ? a : b;
 }
 __device__ __forceinline__ bool tiny(double v) { return v == 0.0 || fabs(v) < TINY; }
+// Ordered loads (asm volatile keeps their issue order): streaming vector loads first, then the
+// solver state, so the state's L2 round trip overlaps the stream instead of gating it.
+__device__ __forceinline__ double ld_stream(const double* p) {
+    double v;
+    asm volatile("ld.global.cs.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ double ld_state(const double* p) {
+    double v;
+    asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ int ld_state(const int* p) {
+    int v;
+    asm volatile("ld.global.cg.s32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
 
 // ---------------------------------------------------------------- mbarrier / bulk copy
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -498,6 +515,9 @@ __global__ void __launch_bounds__(SP_THREADS, MCR_SP_MINB) k_spmv(Csr A, const d
     __syncthreads();
     unsigned long long mb = 0;
     const int G = gridDim.x;
+    // dot partials: each consumer thread adds its rows' terms over ALL its tiles (the static
+    // schedule t = blockIdx.x + i*G fixes the order), one CTA tree at the end -> P[blockIdx.x]
+    double acc1 = 0.0, acc2 = 0.0;
 
     if (warp == SP_CONSUMERS / 32) {
         // ------------------------------------------------------------ producer warp
@@ -602,18 +622,24 @@ __global__ void __launch_bounds__(SP_THREADS, MCR_SP_MINB) k_spmv(Csr A, const d
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty_bar[s]);  // stage free for the producer
             double p1 = 0.0, p2 = 0.0;
-            if (tid < nrows) epi_store<EPI>(V, row, acc, in, p1, p2, mb);
-            if constexpr (epi_has_dot<EPI>()) {
-                p1 = group_sum<SP_CONSUMERS / 32, 1>(p1, s_red);
-                if (tid == 0) V.P1[t] = p1;
-                if constexpr (EPI == EPI_T) {
-                    p2 = group_sum<SP_CONSUMERS / 32, 1>(p2, s_red);
-                    if (tid == 0) V.P2[t] = p2;
+            if (tid < nrows) {
+                epi_store<EPI>(V, row, acc, in, p1, p2, mb);
+                if constexpr (epi_has_dot<EPI>()) {
+                    acc1 = dadd(acc1, p1);
+                    if constexpr (EPI == EPI_T) acc2 = dadd(acc2, p2);
                 }
             }
         }
+        if constexpr (epi_has_dot<EPI>()) {
+            acc1 = group_sum<SP_CONSUMERS / 32, 1>(acc1, s_red);
+            if (tid == 0) V.P1[blockIdx.x] = acc1;
+            if constexpr (EPI == EPI_T) {
+                acc2 = group_sum<SP_CONSUMERS / 32, 1>(acc2, s_red);
+                if (tid == 0) V.P2[blockIdx.x] = acc2;
+            }
+        }
     }
-    kernel_finish<SP_THREADS, EPI, true>(V, st, A.ntiles, mb, s_red, s_redu, &s_flag);
+    kernel_finish<SP_THREADS, EPI, true>(V, st, G, mb, s_red, s_redu, &s_flag);
 }
 
 // Descriptors of the off-diagonal copy's tiles (same row ranges, entry ranges from rrp).
@@ -1000,6 +1026,11 @@ __global__ void __launch_bounds__(SM_NT) k_bicg_small(Csr A, Vecs V, SolveState*
 
 // ---------------------------------------------------------------- element-wise phases
 // BiCGStab vector updates, CHUNK_PER rows per thread (rows strided by CHUNK_NT: coalesced).
+// No phase branches on the stop flag before its loads: a branch would gate the whole stream on
+// the state's L2 round trip (ptxas hoists early exits above side-effect-free loads). Instead a
+// stopped solve is made harmless: p and s are dead once the solve has stopped (only x and the
+// state are read afterwards), so A and C write them unconditionally and C adds to the running
+// max only while live; E rewrites x with its old value and skips its scalar step.
 template <int PH>
 __global__ void __launch_bounds__(CHUNK_NT) k_phase(Vecs V, int n, SolveState* st) {
     __shared__ double s_red[CHUNK_NT / 32];
@@ -1007,7 +1038,6 @@ __global__ void __launch_bounds__(CHUNK_NT) k_phase(Vecs V, int n, SolveState* s
     __shared__ int s_flag;
     griddep_wait();
     griddep_launch();
-    if (st->stop) return;
     const int base = blockIdx.x * CHUNK_ROWS + threadIdx.x;
     if constexpr (PH == PH_A) {
         const double beta = st->beta, w = st->w;
@@ -1024,6 +1054,7 @@ __global__ void __launch_bounds__(CHUNK_NT) k_phase(Vecs V, int n, SolveState* s
         }
     } else if constexpr (PH == PH_C) {
         const double a = st->a;
+        const int stop = st->stop;
         double r[CHUNK_PER], v[CHUNK_PER];
 #pragma unroll
         for (int u = 0; u < CHUNK_PER; ++u) {
@@ -1041,9 +1072,10 @@ __global__ void __launch_bounds__(CHUNK_NT) k_phase(Vecs V, int n, SolveState* s
             }
         }
         mb = group_max<CHUNK_NT / 32, 0>(mb, s_redu);
-        if (threadIdx.x == 0 && mb) atomicMax(&st->maxbits, mb);
+        if (threadIdx.x == 0 && mb && !stop) atomicMax(&st->maxbits, mb);
     } else {
         const double a = st->a, w = st->w;
+        const int stop = st->stop;
         double xv[CHUNK_PER], p[CHUNK_PER], s[CHUNK_PER], t[CHUNK_PER], q[CHUNK_PER];
 #pragma unroll
         for (int u = 0; u < CHUNK_PER; ++u) {
@@ -1054,20 +1086,23 @@ __global__ void __launch_bounds__(CHUNK_NT) k_phase(Vecs V, int n, SolveState* s
             }
         }
         double part = 0.0;
+        const long long keep = stop ? -1ll : 0ll;  // bit select, not a branch (see above)
 #pragma unroll
         for (int u = 0; u < CHUNK_PER; ++u) {
             const int i = base + u * CHUNK_NT;
             if (i < n) {
-                V.x[i] = dadd(dadd(xv[u], dmul(a, p[u])), dmul(w, s[u]));  // x + a p + w s
-                const double rv = dsub(s[u], dmul(w, t[u]));               // r = s - w t
+                const double xn = dadd(dadd(xv[u], dmul(a, p[u])), dmul(w, s[u]));  // x + a p + w s
+                V.x[i] = __longlong_as_double((__double_as_longlong(xn) & ~keep) |
+                                              (__double_as_longlong(xv[u]) & keep));
+                const double rv = dsub(s[u], dmul(w, t[u]));                      // r = s - w t
                 V.r[i] = rv;
-                part = dadd(part, dmul(q[u], rv));                          // q . r
+                part = dadd(part, dmul(q[u], rv));                                 // q . r
             }
         }
         part = group_sum<CHUNK_NT / 32, 0>(part, s_red);
         if (threadIdx.x == 0) V.P1[blockIdx.x] = part;
         if (!last_cta(&st->done, &s_flag)) return;
-        if (st->seqdots) {
+        if (st->seqdots || stop) {
             if (threadIdx.x == 0) st->done = 0;
             return;
         }
