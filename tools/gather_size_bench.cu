@@ -33,12 +33,16 @@ __global__ void __launch_bounds__(256) k_g(const int* __restrict__ col, const do
     for (int o = 16; o; o >>= 1) acc += __shfl_down_sync(~0u, acc, o);
     if (lane == 0) atomicAdd(out, acc);
 }
-int main() {
+int main(int argc, char** argv) {
     const long long NX = 200000000LL, m = 100000000LL;
     double* x; int* col; double* out; char* flush;
     CK(cudaMalloc(&x, NX * 8)); CK(cudaMalloc(&col, m * 4)); CK(cudaMalloc(&out, 8)); CK(cudaMalloc(&flush, 256 << 20));
     CK(cudaMemset(x, 0, NX * 8));
     int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    size_t gran = 0;
+    if (argc > 1) CK(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(argv[1])));
+    CK(cudaDeviceGetLimit(&gran, cudaLimitMaxL2FetchGranularity));
+    printf("cudaLimitMaxL2FetchGranularity = %zu\n", gran);
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     long long ws[] = {1000000, 4000000, 12000000, 16000000, 32000000, 64000000, 100000000, 200000000};
     for (long long w : ws) {
