@@ -26,7 +26,12 @@ __global__ void __launch_bounds__(256) k_g(const int* __restrict__ col, const do
 #pragma unroll
         for (int u = 0; u < 8; ++u) cc[u] = __ldcs(col + b + 32 * u);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) xv[u] = __ldg(x + cc[u]);
+        for (int u = 0; u < 8; ++u) {
+            if (SORTED == 1) asm volatile("ld.global.nc.L2::64B.f64 %0, [%1];" : "=d"(xv[u]) : "l"(x + cc[u]));
+            else if (SORTED == 2) asm volatile("ld.global.nc.L2::256B.f64 %0, [%1];" : "=d"(xv[u]) : "l"(x + cc[u]));
+            else if (SORTED == 3) asm volatile("ld.global.nc.L1::no_allocate.L2::64B.f64 %0, [%1];" : "=d"(xv[u]) : "l"(x + cc[u]));
+            else xv[u] = __ldg(x + cc[u]);
+        }
 #pragma unroll
         for (int u = 0; u < 8; ++u) acc += xv[u];
     }
@@ -44,7 +49,8 @@ int main(int argc, char** argv) {
     CK(cudaDeviceGetLimit(&gran, cudaLimitMaxL2FetchGranularity));
     printf("cudaLimitMaxL2FetchGranularity = %zu\n", gran);
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-    long long ws[] = {1000000, 4000000, 12000000, 16000000, 32000000, 64000000, 100000000, 200000000};
+    long long ws[] = {4000000, 32000000, 200000000};
+    for (int mode = 0; mode < 4; ++mode)
     for (long long w : ws) {
         k_init<<<4096, 256>>>(col, m, w);
         CK(cudaDeviceSynchronize());
@@ -52,13 +58,16 @@ int main(int argc, char** argv) {
         for (int r = 0; r < 5; ++r) {
             CK(cudaMemset(flush, r, 256 << 20));
             cudaEventRecord(e0);
-            k_g<0><<<sms * 4, 256>>>(col, x, m, out);
+            if (mode == 0) k_g<0><<<sms * 4, 256>>>(col, x, m, out);
+            if (mode == 1) k_g<1><<<sms * 4, 256>>>(col, x, m, out);
+            if (mode == 2) k_g<2><<<sms * 4, 256>>>(col, x, m, out);
+            if (mode == 3) k_g<3><<<sms * 4, 256>>>(col, x, m, out);
             cudaEventRecord(e1);
             CK(cudaEventSynchronize(e1));
             float ms; cudaEventElapsedTime(&ms, e0, e1);
             if (r >= 1 && ms < best) best = ms;
         }
-        printf("window %10lld doubles (%7.1f MB): %8.2f us  %6.1f Ggather/s\n", w, w * 8 / 1e6, best * 1e3, m / (best * 1e-3) / 1e9);
+        printf("mode %d window %10lld doubles (%7.1f MB): %8.2f us  %6.1f Ggather/s\n", mode, w, w * 8 / 1e6, best * 1e3, m / (best * 1e-3) / 1e9);
     }
     return 0;
 }
