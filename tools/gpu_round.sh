@@ -1,11 +1,13 @@
 #!/bin/bash
-# One GPU-box pass: parity tests, smoke, bench, ncu launch list + full capture of the SpMV.
+# One GPU-box pass: parity tests, smoke, bench (ours + reference arm), ncu launch list + full
+# capture of the SpMV. Outputs under gpurun_out/.
 cd "$GRAFT_REPO_ROOT" || exit 1
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/gpu.txt 2>&1
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 timeout 300 python __graft_entry__.py > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
 timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
+timeout 600 python bench.py --impl reference --steps 1 --warmup 0 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/bench_ncu.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_spmv -c 3 -o gpurun_out/spmv_full -f python tools/prof_spmv.py --mv 3 --jit 0 --bit 0 > gpurun_out/ncu_full.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k k_spmv -c 3 -o gpurun_out/spmv_full -f python tools/prof_spmv.py --mv 3 --jit 0 --bit 0 > gpurun_out/ncu_full.log 2>&1
 echo done
