@@ -190,6 +190,35 @@ MCR_API int mcr_generate_rhs(const mcr_matrix* m, uint64_t seed, double* d_b);
  * nonzero[nnz]); any pointer may be NULL. */
 MCR_API int mcr_matrix_export(mcr_matrix* m, int64_t* rstart, int64_t* col, double* nonzero);
 
+/* ---------------------------------------------------------------------------------------
+ * Reachability of a Markov chain: the caller side of the solve,
+ * build_system + reachability_probabilities (markov.py:152-293), on the device.
+ *   mcr_chain_create  uploads the transitions (CSR, rows sorted by target) and the goal states,
+ *                     partitions the states with two backward closures (prob 0 / prob 1 /
+ *                     uncertain), and assembles M = I - A over the uncertain states (ascending)
+ *                     and rhs = one-step goal probability -- bit-identical to the reference.
+ *   mcr_chain_export  host copies: classes[n] (0 = prob zero, 1 = prob one, 2 = uncertain),
+ *                     uncertain[k], M (k+1 / m / m) and rhs[k]; any pointer may be NULL.
+ *   mcr_chain_matrix  the solve-ready handle of M (owned by the chain: do not destroy).
+ *   mcr_chain_solve   method 0 Jacobi / 1 BiCGStab (dots 1 = reference-order inner products)
+ *                     on M x = rhs; on success x_out[n] = 1 on prob-one states, 0 on prob-zero
+ *                     states, clip(x, 0, 1) on the uncertain ones. xs_out[k] receives the
+ *                     reduced solution (also on NotConverged / Breakdown). Status as mcr_jacobi.
+ * ------------------------------------------------------------------------------------- */
+typedef struct mcr_chain mcr_chain;
+MCR_API int mcr_chain_create(int64_t n, const int64_t* rstart, const int64_t* col,
+                             const double* prob, const int64_t* goals, int64_t ngoals, int device,
+                             mcr_chain** out);
+MCR_API void mcr_chain_destroy(mcr_chain* chain);
+MCR_API int mcr_chain_info(const mcr_chain* chain, int64_t* uncertain, int64_t* prob_one,
+                           int64_t* prob_zero, int64_t* m_nnz);
+MCR_API int mcr_chain_export(mcr_chain* chain, int8_t* classes, int64_t* uncertain,
+                             int64_t* m_rstart, int64_t* m_col, double* m_nonzero, double* rhs);
+MCR_API int mcr_chain_matrix(mcr_chain* chain, mcr_matrix** out);
+MCR_API int mcr_chain_solve(mcr_chain* chain, int method, int dots, double tol,
+                            int64_t max_iterations, double* x_out, double* xs_out,
+                            mcr_report* report);
+
 /* Message of the last failing call on this thread ("" if none). */
 MCR_API const char* mcr_last_error(void);
 

@@ -30,7 +30,8 @@ EXPORTS = (
     "mcr_bicgstab_device", "mcr_last_error", "mcr_set_dot_mode",
     "mcr_shard_rows", "mcr_comm_unique_id", "mcr_comm_create_nccl", "mcr_comm_create_local",
     "mcr_comm_destroy", "mcr_comm_info", "mcr_shard_create", "mcr_generate",
-    "mcr_generate_rhs", "mcr_matrix_export",
+    "mcr_generate_rhs", "mcr_matrix_export", "mcr_chain_create", "mcr_chain_destroy",
+    "mcr_chain_info", "mcr_chain_export", "mcr_chain_matrix", "mcr_chain_solve",
 )
 COMM_ID_BYTES = 128
 DOTS_TREE, DOTS_SEQUENTIAL = 0, 1
@@ -116,6 +117,13 @@ def load():
     L.mcr_generate.argtypes = [vp, ip, i64, dbl, ip, ip, ctypes.c_uint64, ip, ctypes.POINTER(vp)]
     L.mcr_generate_rhs.argtypes = [vp, ctypes.c_uint64, vp]
     L.mcr_matrix_export.argtypes = [vp, vp, vp, vp]
+    L.mcr_chain_create.argtypes = [i64, vp, vp, vp, vp, i64, ip, ctypes.POINTER(vp)]
+    L.mcr_chain_destroy.argtypes = [vp]
+    L.mcr_chain_destroy.restype = None
+    L.mcr_chain_info.argtypes = [vp, pi64, pi64, pi64, pi64]
+    L.mcr_chain_export.argtypes = [vp, vp, vp, vp, vp, vp, vp]
+    L.mcr_chain_matrix.argtypes = [vp, ctypes.POINTER(vp)]
+    L.mcr_chain_solve.argtypes = [vp, ip, ip, dbl, i64, vp, vp, ctypes.POINTER(Report)]
     L.mcr_last_error.restype = ctypes.c_char_p
     L.mcr_last_error.argtypes = []
     _lib = L

@@ -23,6 +23,7 @@
 
 #include "comm.h"
 #include "device.cuh"
+#include "chain.cuh"
 #include "generator.cuh"
 #include "mcr.h"
 
@@ -63,6 +64,31 @@ struct DeviceGuard {
 enum { V_X = 0, V_X1, V_P, V_S, V_FULL_COUNT, V_B = V_FULL_COUNT, V_R, V_Q, V_V, V_T, V_COUNT };
 
 }  // namespace
+
+struct mcr_matrix;
+
+// A Markov chain with its goal set and the reduced system built from it (chain.cuh).
+struct mcr_chain {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int64_t n = 0, nnz = 0, k = 0, m_nnz = 0, nzero = 0, none = 0;
+    long long* rp = nullptr;
+    int* col = nullptr;
+    double* val = nullptr;
+    unsigned char* goal = nullptr;
+    signed char* cls = nullptr;
+    long long* remap = nullptr;
+    long long* list = nullptr;
+    long long* mrp = nullptr;
+    int* mcol = nullptr;
+    double* mval = nullptr;
+    double* rhs = nullptr;
+    double* xs = nullptr;
+    double* xfull = nullptr;
+    mcr_matrix* M = nullptr;  // solve-ready handle of M (created on first use)
+    std::vector<void*> owned;
+    std::mutex mu;
+};
 
 // Communicator of a row-sharded solve (comm.h): NCCL, or the in-process local group.
 struct mcr_comm {
@@ -734,6 +760,37 @@ static int create_impl(mcr_matrix* h, int64_t n, const int64_t* rs, const int64_
     return finish_create(h, n, rs, storage);
 }
 
+// A handle from a CSR already on the device (int64 row starts, int32 columns), copied.
+static int create_from_device(int64_t n, int64_t nnz, const long long* d_rp, const int* d_col,
+                              const double* d_val, int device, int storage, mcr_matrix** out) {
+    DeviceGuard g(device);
+    mcr_matrix* h = new mcr_matrix();
+    h->device = device;
+    h->n = n;
+    h->n_global = n;
+    h->chunk = n;
+    int rc = [&]() -> int {
+        TRY(init_handle(h));
+        if (n == 0) return MCR_OK;
+        TRY(alloc_csr(h, n, nnz));
+        CK(cudaMemcpyAsync(h->rp, d_rp, sizeof(long long) * (size_t)(n + 1), cudaMemcpyDeviceToDevice, h->stream));
+        CK(cudaMemcpyAsync(h->col, d_col, sizeof(int) * (size_t)nnz, cudaMemcpyDeviceToDevice, h->stream));
+        CK(cudaMemcpyAsync(h->val, d_val, sizeof(double) * (size_t)nnz, cudaMemcpyDeviceToDevice, h->stream));
+        std::vector<int64_t> rs((size_t)n + 1);
+        CK(cudaMemcpyAsync(rs.data(), d_rp, sizeof(int64_t) * rs.size(), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        return finish_create(h, n, rs.data(), storage);
+    }();
+    if (rc != MCR_OK) {
+        std::string msg = g_err;
+        mcr_matrix_destroy(h);
+        g_err = msg;
+        return rc;
+    }
+    *out = h;
+    return MCR_OK;
+}
+
 // Poisson(mean) inverse-CDF thresholds on 2^64 (generator.cuh); restated in oracle.c.
 static void poisson_thresholds(double mean, uint64_t* thr) {
     double p = std::exp(-mean), cdf = 0.0;
@@ -1098,6 +1155,301 @@ MCR_API int mcr_matrix_export(mcr_matrix* h, int64_t* rstart, int64_t* col, doub
     }
     CK(cudaStreamSynchronize(h->stream));
     return MCR_OK;
+}
+
+// ---------------------------------------------------------------- chains (build_system)
+}  // extern "C" (helpers below are C++)
+
+template <class T>
+static int calloc_owned(mcr_chain* c, T** p, size_t count) {
+    *p = nullptr;
+    CK(cudaMallocAsync((void**)p, sizeof(T) * std::max<size_t>(count, 1), c->stream));
+    c->owned.push_back((void*)*p);
+    return MCR_OK;
+}
+
+static int chain_scan(mcr_chain* c, const long long* in, long long* out, int64_t count) {
+    size_t tmp = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, count, c->stream));
+    void* d = nullptr;
+    CK(cudaMallocAsync(&d, std::max<size_t>(tmp, 1), c->stream));
+    CK(cub::DeviceScan::ExclusiveSum(d, tmp, in, out, count, c->stream));
+    CK(cudaFreeAsync(d, c->stream));
+    return MCR_OK;
+}
+
+// Backward closure (k_closure) from states with flag == want, never entering blocked states.
+static int chain_closure(mcr_chain* c, const unsigned long long* rev_rp, const int* rev_src,
+                         const unsigned char* flag, unsigned char want,
+                         const unsigned char* blocked, int* seen, int* fa, int* fb, unsigned* len) {
+    const int n = (int)c->n;
+    CK(cudaMemsetAsync(seen, 0, sizeof(int) * (size_t)n, c->stream));
+    CK(cudaMemsetAsync(len, 0, sizeof(unsigned) * 3, c->stream));
+    const int g = (int)std::min<int64_t>((n + 255) / 256, 4096);
+    k_seed<<<g, 256, 0, c->stream>>>(flag, want, n, seen, fa, len);
+    CK(cudaGetLastError());
+    int sms = 0, per = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_closure, 256, 0));
+    void* args[] = {(void*)&rev_rp, (void*)&rev_src, (void*)&blocked, (void*)&seen, (void*)&fa,
+                    (void*)&fb, (void*)&len};
+    CK(cudaLaunchCooperativeKernel((void*)k_closure, sms * std::max(1, per), 256, args, 0, c->stream));
+    return MCR_OK;
+}
+
+static int chain_build(mcr_chain* c, const int64_t* rstart, const int64_t* col, const double* prob,
+                       const int64_t* goals, int64_t ngoals) {
+    const int64_t n = c->n, nnz = c->nnz;
+    cudaStream_t s = c->stream;
+    TRY(calloc_owned(c, &c->rp, (size_t)n + 1));
+    TRY(calloc_owned(c, &c->col, (size_t)nnz));
+    TRY(calloc_owned(c, &c->val, (size_t)nnz));
+    TRY(calloc_owned(c, &c->goal, (size_t)n));
+    TRY(calloc_owned(c, &c->cls, (size_t)n));
+    TRY(calloc_owned(c, &c->remap, (size_t)n + 1));
+    CK(cudaMemcpyAsync(c->rp, rstart, sizeof(long long) * (size_t)(n + 1), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(c->val, prob, sizeof(double) * (size_t)nnz, cudaMemcpyHostToDevice, s));
+    {
+        std::vector<int> c32((size_t)nnz);
+        for (int64_t e = 0; e < nnz; ++e) {
+            if (col[e] < 0 || col[e] >= n) return fail(MCR_DIMENSION, "transition target out of range");
+            c32[(size_t)e] = (int)col[e];
+        }
+        std::vector<unsigned char> gm((size_t)n, 0);
+        for (int64_t i = 0; i < ngoals; ++i) gm[(size_t)goals[i]] = 1;
+        CK(cudaMemcpyAsync(c->col, c32.data(), sizeof(int) * (size_t)nnz, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(c->goal, gm.data(), (size_t)n, cudaMemcpyHostToDevice, s));
+        CK(cudaStreamSynchronize(s));
+    }
+    // reversed digraph
+    unsigned long long *cnt = nullptr, *rev_rp = nullptr, *cursor = nullptr;
+    int *rev_src = nullptr, *seen_goal = nullptr, *seen_zero = nullptr, *fa = nullptr, *fb = nullptr;
+    unsigned* len = nullptr;
+    unsigned char* zero_flag = nullptr;
+    CK(cudaMallocAsync((void**)&cnt, sizeof(*cnt) * (size_t)(n + 1), s));
+    CK(cudaMallocAsync((void**)&rev_rp, sizeof(*rev_rp) * (size_t)(n + 1), s));
+    CK(cudaMallocAsync((void**)&cursor, sizeof(*cursor) * (size_t)n, s));
+    CK(cudaMallocAsync((void**)&rev_src, sizeof(*rev_src) * (size_t)std::max<int64_t>(nnz, 1), s));
+    CK(cudaMallocAsync((void**)&seen_goal, sizeof(int) * (size_t)n, s));
+    CK(cudaMallocAsync((void**)&seen_zero, sizeof(int) * (size_t)n, s));
+    CK(cudaMallocAsync((void**)&fa, sizeof(int) * (size_t)n, s));
+    CK(cudaMallocAsync((void**)&fb, sizeof(int) * (size_t)n, s));
+    CK(cudaMallocAsync((void**)&len, sizeof(unsigned) * 3, s));
+    CK(cudaMallocAsync((void**)&zero_flag, (size_t)n, s));
+    CK(cudaMemsetAsync(cnt, 0, sizeof(*cnt) * (size_t)(n + 1), s));
+    CK(cudaMemsetAsync(cursor, 0, sizeof(*cursor) * (size_t)n, s));
+    const int ge = (int)std::min<int64_t>((nnz + 255) / 256, 1 << 16);
+    const int gn = (int)std::min<int64_t>((n + 255) / 256, 1 << 16);
+    if (nnz) k_rev_count<<<ge, 256, 0, s>>>(c->rp, c->col, nnz, cnt);
+    {
+        size_t tmp = 0;
+        CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, rev_rp, n + 1, s));
+        void* d = nullptr;
+        CK(cudaMallocAsync(&d, std::max<size_t>(tmp, 1), s));
+        CK(cub::DeviceScan::ExclusiveSum(d, tmp, cnt, rev_rp, n + 1, s));
+        CK(cudaFreeAsync(d, s));
+    }
+    k_rev_fill<<<gn, 256, 0, s>>>(c->rp, c->col, (int)n, rev_rp, cursor, rev_src);
+    CK(cudaGetLastError());
+    // states that reach a goal; the rest have probability zero
+    TRY(chain_closure(c, rev_rp, rev_src, c->goal, 1, nullptr, seen_goal, fa, fb, len));
+    // probability zero = no path to a goal; then the closure of that set avoiding the goals
+    k_zero_flag<<<gn, 256, 0, s>>>(seen_goal, (int)n, zero_flag);
+    CK(cudaGetLastError());
+    TRY(chain_closure(c, rev_rp, rev_src, zero_flag, 1, c->goal, seen_zero, fa, fb, len));
+    long long* unc = nullptr;
+    CK(cudaMallocAsync((void**)&unc, sizeof(long long) * (size_t)(n + 1), s));
+    k_classes<<<gn, 256, 0, s>>>(seen_goal, seen_zero, (int)n, c->cls, unc);
+    CK(cudaGetLastError());
+    CK(cudaMemsetAsync(unc + n, 0, sizeof(long long), s));
+    TRY(chain_scan(c, unc, c->remap, n + 1));
+    CK(cudaFreeAsync(unc, s));
+    long long k = 0;
+    CK(cudaMemcpyAsync(&k, c->remap + n, sizeof(k), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    c->k = k;
+    TRY(calloc_owned(c, &c->list, (size_t)k));
+    k_uncertain_list<<<gn, 256, 0, s>>>(c->cls, (int)n, c->remap, c->list);
+    CK(cudaGetLastError());
+    // M = I - A and the one-step goal probabilities
+    long long *mlen = nullptr, *glen = nullptr, *goff = nullptr;
+    double* gsel = nullptr;
+    CK(cudaMallocAsync((void**)&mlen, sizeof(long long) * (size_t)(k + 1), s));
+    CK(cudaMallocAsync((void**)&glen, sizeof(long long) * (size_t)(k + 1), s));
+    CK(cudaMallocAsync((void**)&goff, sizeof(long long) * (size_t)(k + 1), s));
+    TRY(calloc_owned(c, &c->mrp, (size_t)k + 1));
+    TRY(calloc_owned(c, &c->rhs, (size_t)k));
+    CK(cudaMemsetAsync(mlen + k, 0, sizeof(long long), s));
+    CK(cudaMemsetAsync(glen + k, 0, sizeof(long long), s));
+    const int gk = (int)std::min<int64_t>((k + 255) / 256, 1 << 16);
+    if (k) k_m_count<<<gk, 256, 0, s>>>(c->rp, c->col, c->val, c->list, k, c->remap, c->goal, mlen, glen);
+    TRY(chain_scan(c, mlen, c->mrp, k + 1));
+    TRY(chain_scan(c, glen, goff, k + 1));
+    long long mnnz = 0, gtot = 0;
+    CK(cudaMemcpyAsync(&mnnz, c->mrp + k, sizeof(mnnz), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&gtot, goff + k, sizeof(gtot), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    c->m_nnz = mnnz;
+    TRY(calloc_owned(c, &c->mcol, (size_t)mnnz));
+    TRY(calloc_owned(c, &c->mval, (size_t)mnnz));
+    CK(cudaMallocAsync((void**)&gsel, sizeof(double) * (size_t)std::max<long long>(gtot, 1), s));
+    if (k) {
+        k_m_fill<<<gk, 256, 0, s>>>(c->rp, c->col, c->val, c->list, k, c->remap, c->goal, c->mrp,
+                                    c->mcol, c->mval, goff, gsel);
+        k_rhs<<<gk, 256, 0, s>>>(goff, k, gsel, c->rhs);
+    }
+    CK(cudaGetLastError());
+    for (void* p : {(void*)cnt, (void*)rev_rp, (void*)cursor, (void*)rev_src, (void*)seen_goal,
+                    (void*)seen_zero, (void*)fa, (void*)fb, (void*)len, (void*)zero_flag,
+                    (void*)mlen, (void*)glen, (void*)goff, (void*)gsel})
+        CK(cudaFreeAsync(p, s));
+    // class counts
+    std::vector<signed char> cls((size_t)n);
+    CK(cudaMemcpyAsync(cls.data(), c->cls, (size_t)n, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    c->nzero = c->none = 0;
+    for (signed char v : cls) {
+        c->nzero += v == 0;
+        c->none += v == 1;
+    }
+    return MCR_OK;
+}
+
+extern "C" {
+
+MCR_API void mcr_chain_destroy(mcr_chain* c) {
+    if (!c) return;
+    {
+        DeviceGuard g(c->device);
+        if (c->M) mcr_matrix_destroy(c->M);
+        for (void* p : c->owned) cudaFreeAsync(p, c->stream);
+        if (c->stream) {
+            cudaStreamSynchronize(c->stream);
+            cudaStreamDestroy(c->stream);
+        }
+    }
+    delete c;
+}
+
+MCR_API int mcr_chain_create(int64_t n, const int64_t* rstart, const int64_t* col,
+                             const double* prob, const int64_t* goals, int64_t ngoals, int device,
+                             mcr_chain** out) {
+    if (!out) return fail(MCR_INVALID_ARGUMENT, "out is NULL");
+    *out = nullptr;
+    if (n < 1 || n >= INT_MAX) return fail(MCR_DIMENSION, "a chain needs 1 <= n < 2^31 states");
+    TRY(check_csr(n, rstart, col, prob));
+    if (ngoals < 1 || !goals) return fail(MCR_INVALID_ARGUMENT, "goal set must not be empty");
+    for (int64_t i = 0; i < ngoals; ++i)
+        if (goals[i] < 0 || goals[i] >= n)
+            return fail(MCR_DIMENSION, "goal state " + std::to_string(goals[i]) + " out of range");
+    int ndev = 0;
+    mcr_device_count(&ndev);
+    if (device < 0 || device >= ndev) return fail(MCR_CUDA_ERROR, "no CUDA device " + std::to_string(device));
+    DeviceGuard g(device);
+    TRY(keep_pool_memory(device));
+    mcr_chain* c = new mcr_chain();
+    c->device = device;
+    c->n = n;
+    c->nnz = rstart[n];
+    int rc = MCR_OK;
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess)
+        rc = fail(MCR_CUDA_ERROR, "cudaStreamCreate failed");
+    if (rc == MCR_OK) rc = chain_build(c, rstart, col, prob, goals, ngoals);
+    if (rc != MCR_OK) {
+        std::string msg = g_err;
+        mcr_chain_destroy(c);
+        g_err = msg;
+        return rc;
+    }
+    *out = c;
+    return MCR_OK;
+}
+
+MCR_API int mcr_chain_info(const mcr_chain* c, int64_t* uncertain, int64_t* prob_one,
+                           int64_t* prob_zero, int64_t* m_nnz) {
+    if (!c) return fail(MCR_INVALID_ARGUMENT, "NULL chain");
+    if (uncertain) *uncertain = c->k;
+    if (prob_one) *prob_one = c->none;
+    if (prob_zero) *prob_zero = c->nzero;
+    if (m_nnz) *m_nnz = c->m_nnz;
+    return MCR_OK;
+}
+
+MCR_API int mcr_chain_export(mcr_chain* c, int8_t* classes, int64_t* uncertain, int64_t* m_rstart,
+                             int64_t* m_col, double* m_nonzero, double* rhs) {
+    if (!c) return fail(MCR_INVALID_ARGUMENT, "NULL chain");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    cudaStream_t s = c->stream;
+    const size_t k = (size_t)c->k, m = (size_t)c->m_nnz;
+    if (classes) CK(cudaMemcpyAsync(classes, c->cls, (size_t)c->n, cudaMemcpyDeviceToHost, s));
+    if (uncertain && k) CK(cudaMemcpyAsync(uncertain, c->list, sizeof(int64_t) * k, cudaMemcpyDeviceToHost, s));
+    if (m_rstart) CK(cudaMemcpyAsync(m_rstart, c->mrp, sizeof(int64_t) * (k + 1), cudaMemcpyDeviceToHost, s));
+    if (m_nonzero && m) CK(cudaMemcpyAsync(m_nonzero, c->mval, sizeof(double) * m, cudaMemcpyDeviceToHost, s));
+    if (rhs && k) CK(cudaMemcpyAsync(rhs, c->rhs, sizeof(double) * k, cudaMemcpyDeviceToHost, s));
+    std::vector<int> c32(m_col ? m : 0);
+    if (m_col && m) CK(cudaMemcpyAsync(c32.data(), c->mcol, sizeof(int) * m, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (size_t e = 0; m_col && e < m; ++e) m_col[e] = c32[e];
+    return MCR_OK;
+}
+
+MCR_API int mcr_chain_matrix(mcr_chain* c, mcr_matrix** out) {
+    if (!c || !out) return fail(MCR_INVALID_ARGUMENT, "NULL argument");
+    std::lock_guard<std::mutex> lk(c->mu);
+    *out = nullptr;
+    if (!c->M) {
+        CK(cudaStreamSynchronize(c->stream));
+        TRY(create_from_device(c->k, c->m_nnz, c->mrp, c->mcol, c->mval, c->device,
+                               MCR_STORAGE_AUTO, &c->M));
+    }
+    *out = c->M;
+    return MCR_OK;
+}
+
+MCR_API int mcr_chain_solve(mcr_chain* c, int method, int dots, double tol, int64_t max_it,
+                            double* x_out, double* xs_out, mcr_report* rep) {
+    if (!c || !rep) return fail(MCR_INVALID_ARGUMENT, "NULL argument");
+    if (method != 0 && method != 1) return fail(MCR_INVALID_ARGUMENT, "method: 0 jacobi, 1 bicgstab");
+    if (!(tol > 0.0)) return fail(MCR_INVALID_ARGUMENT, "tolerance must be positive");
+    if (max_it < 1) return fail(MCR_INVALID_ARGUMENT, "max_iterations must be at least 1");
+    report_init(rep);
+    DeviceGuard g(c->device);
+    if (c->k == 0) {  // no uncertain state: nothing to solve (markov.py:287-288)
+        rep->converged = 1;
+        if (x_out) {
+            std::vector<signed char> cls((size_t)c->n);
+            CK(cudaMemcpyAsync(cls.data(), c->cls, (size_t)c->n, cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+            for (int64_t s = 0; s < c->n; ++s) x_out[s] = cls[(size_t)s] == 1 ? 1.0 : 0.0;
+        }
+        return MCR_OK;
+    }
+    mcr_matrix* M = nullptr;
+    TRY(mcr_chain_matrix(c, &M));
+    TRY(mcr_set_dot_mode(M, dots ? MCR_DOTS_SEQUENTIAL : MCR_DOTS_TREE));
+    std::lock_guard<std::mutex> lk(M->mu);
+    {
+        std::lock_guard<std::mutex> lc(c->mu);
+        if (!c->xs) TRY(calloc_owned(c, &c->xs, (size_t)c->k));
+        if (!c->xfull) TRY(calloc_owned(c, &c->xfull, (size_t)c->n));
+        CK(cudaStreamSynchronize(c->stream));
+    }
+    const int rc = method == 0 ? jacobi_impl(M, c->rhs, nullptr, tol, max_it, c->xs, rep)
+                               : bicgstab_impl(M, c->rhs, nullptr, tol, max_it, c->xs, rep);
+    if (rc != MCR_OK && rc != MCR_NOT_CONVERGED && rc != MCR_BREAKDOWN) return rc;
+    const std::string msg = g_err;
+    if (xs_out)
+        CK(cudaMemcpyAsync(xs_out, c->xs, sizeof(double) * (size_t)c->k, cudaMemcpyDeviceToHost, M->stream));
+    if (x_out && rc == MCR_OK) {
+        k_scatter_x<<<(int)std::min<int64_t>((c->n + 255) / 256, 1 << 16), 256, 0, M->stream>>>(
+            c->cls, c->remap, c->xs, (int)c->n, c->xfull);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(x_out, c->xfull, sizeof(double) * (size_t)c->n, cudaMemcpyDeviceToHost, M->stream));
+    }
+    CK(cudaStreamSynchronize(M->stream));
+    g_err = msg;
+    return rc;
 }
 
 MCR_API int mcr_matrix_info_get(const mcr_matrix* h, mcr_matrix_info* info) {
