@@ -9,5 +9,5 @@ timeout 300 python __graft_entry__.py > gpurun_out/smoke.log 2>&1; echo "smoke r
 timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
 timeout 600 python bench.py --impl reference --steps 1 --warmup 0 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/bench_ncu.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k k_spmv -c 3 -o gpurun_out/spmv_full -f python tools/prof_spmv.py --mv 3 --jit 0 --bit 0 > gpurun_out/ncu_full.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k k_spmv -c 6 -o gpurun_out/spmv_full -f python tools/prof_spmv.py --mv 2 --jit 3 --bit 0 > gpurun_out/ncu_full.log 2>&1
 echo done
