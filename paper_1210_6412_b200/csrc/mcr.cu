@@ -703,7 +703,8 @@ static int set_kernel_attributes() {
 
 // Rows [h->roff, h->roff + n) of an h->n_global system (the whole system on one GPU);
 // column indices are global.
-static int finish_create(mcr_matrix* h, int64_t n, const int64_t* rs, int storage);
+static int finish_create(mcr_matrix* h, int64_t n, const int64_t* rs, int storage,
+                         std::vector<int>* pre_tiles = nullptr);
 
 static int init_handle(mcr_matrix* h) {
     TRY(keep_pool_memory(h->device));
@@ -754,10 +755,12 @@ static int create_impl(mcr_matrix* h, int64_t n, const int64_t* rs, const int64_
         CK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
         CK(cudaFreeAsync(tmp, h->stream));
         CK(cudaFreeAsync(bad, h->stream));
+        // the row tiles are cut on the host while the copies are in flight
+        std::vector<int> tiles = make_tiles(n, rs, &h->max_row);
         CK(cudaStreamSynchronize(h->stream));
         if (hbad) return fail(MCR_DIMENSION, "column index out of range");
+        return finish_create(h, n, rs, storage, &tiles);
     }
-    return finish_create(h, n, rs, storage);
 }
 
 // A handle from a CSR already on the device (int64 row starts, int32 columns), copied.
@@ -834,7 +837,8 @@ static int generate_impl(mcr_matrix* h, const GenParams& P, int storage) {
 
 // Device CSR (rp/col/val) in place; `rs` = host copy of the row starts. Diagonal, tiles or
 // dense slabs, kernel attributes.
-static int finish_create(mcr_matrix* h, int64_t n, const int64_t* rs, int storage) {
+static int finish_create(mcr_matrix* h, int64_t n, const int64_t* rs, int storage,
+                         std::vector<int>* pre_tiles) {
     const int64_t nnz = h->nnz;
     const bool dense = !h->sharded() &&
                        (storage == MCR_STORAGE_DENSE ||
@@ -856,7 +860,9 @@ static int finish_create(mcr_matrix* h, int64_t n, const int64_t* rs, int storag
         CK(cudaStreamSynchronize(h->stream));
         h->first_zero = hfz == ~0ull ? -1 : (long long)hfz + h->roff;  // global row
     }
-    std::vector<int> tiles = make_tiles(n, rs, &h->max_row);
+    std::vector<int> tiles;
+    if (pre_tiles) tiles.swap(*pre_tiles);
+    else tiles = make_tiles(n, rs, &h->max_row);
     if (dense) {
         h->nslabs = (int)((n + DSLAB - 1) / DSLAB);
         const int64_t npad = (n + 1) & ~1ll;  // column pairs
