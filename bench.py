@@ -472,6 +472,8 @@ def run_c5(args):
     if world > 1:
         comm = Comm.nccl(local)
         h = ShardMatrix.generated(comm, n, mean, 1, 10, seed)
+        if args.p2p:
+            h.enable_p2p()
     else:
         comm = None
         h = DeviceMatrix.generated(n, mean, 1, 10, seed, device=local, storage=_lib.STORAGE_TILES)
@@ -583,7 +585,9 @@ def run_c5(args):
                    "n": n, "nnz": nnz, "tolerance": 1e-10,
                    "solve_pair": "jacobi + bicgstab (tree dots) from x0=0",
                    "l2": "inputs (x 1.6 GB, matrix ~19 GB) far larger than L2",
-                   "parallelism": f"row shards x{world} (NCCL allgather + rank-order reductions)",
+                   "parallelism": (f"row shards x{world} ("
+                                   + ("fused P2P stores + NCCL slot exchange" if args.p2p and world > 1
+                                      else "NCCL allgather + rank-order reductions") + ")"),
                    "generation_s": t_gen},
         "iterations": iters,
         "time_to_solution_ms": {"jacobi": rj.device_seconds * 1e3, "bicgstab": rb.device_seconds * 1e3},
@@ -614,6 +618,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c5"])
     ap.add_argument("--n", type=int, default=2 * 10 ** 8, help="C5 dimension")
+    ap.add_argument("--p2p", action="store_true",
+                    help="C5 at N > 1: fused exchange (producers store into peers' copies)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":

@@ -172,6 +172,14 @@ MCR_API int mcr_shard_create(mcr_comm* comm, int64_t n_global, int64_t row0, int
                              const int64_t* rstart, const int64_t* col, const double* nonzero,
                              mcr_matrix** out);
 
+/* Fused exchange for a row shard (collective: every rank calls it, before its first solve):
+ * the full vectors that SpMVs gather (Jacobi iterates, BiCGStab p and s) move to an
+ * IPC-exportable allocation mapped into every peer (cudaIpc* across processes, plain pointers
+ * within one); the kernels that produce those vectors store each own-row value into every
+ * peer's copy as they compute it, so the allgather rides NVLink inside the producer instead
+ * of following it, and the per-sweep collective shrinks to the SEND_SLOTS exchange. */
+MCR_API int mcr_shard_enable_p2p(mcr_matrix* shard);
+
 /* ---------------------------------------------------------------------------------------
  * Synthetic systems built directly in HBM (config C5: n = 2e8 does not fit the reference's
  * host generator). Family of generate_dd_matrix / generate_rhs (generator.py:100-132):

@@ -32,6 +32,7 @@ EXPORTS = (
     "mcr_comm_destroy", "mcr_comm_info", "mcr_shard_create", "mcr_generate",
     "mcr_generate_rhs", "mcr_matrix_export", "mcr_chain_create", "mcr_chain_destroy",
     "mcr_chain_info", "mcr_chain_export", "mcr_chain_matrix", "mcr_chain_solve",
+    "mcr_shard_enable_p2p",
 )
 COMM_ID_BYTES = 128
 DOTS_TREE, DOTS_SEQUENTIAL = 0, 1
@@ -117,6 +118,7 @@ def load():
     L.mcr_generate.argtypes = [vp, ip, i64, dbl, ip, ip, ctypes.c_uint64, ip, ctypes.POINTER(vp)]
     L.mcr_generate_rhs.argtypes = [vp, ctypes.c_uint64, vp]
     L.mcr_matrix_export.argtypes = [vp, vp, vp, vp]
+    L.mcr_shard_enable_p2p.argtypes = [vp]
     L.mcr_chain_create.argtypes = [i64, vp, vp, vp, vp, i64, ip, ctypes.POINTER(vp)]
     L.mcr_chain_destroy.argtypes = [vp]
     L.mcr_chain_destroy.restype = None

@@ -20,6 +20,7 @@
 #include <nccl.h>
 
 #include <chrono>
+#include <cstring>
 #include <condition_variable>
 #include <memory>
 #include <mutex>
@@ -45,6 +46,10 @@ struct Transport {
         return rc ? rc : gather_slots(send, recv, slots, s);
     }
     virtual const char* kind() const = 0;
+    // Host-level allgather of `bytes` per rank (setup only: peer mappings).
+    virtual int share_bytes(const void* mine, void* all, size_t bytes) = 0;
+    // Ranks live in this process (peer buffers are plain device pointers, no IPC).
+    virtual bool same_process() const = 0;
 };
 
 // ------------------------------------------------------------------------------- NCCL
@@ -128,6 +133,30 @@ struct NcclTransport : Transport {
         return rc ? rc : rc2;
     }
     const char* kind() const override { return "nccl"; }
+    int share_bytes(const void* mine, void* all, size_t bytes) override {
+        char* d = nullptr;
+        cudaStream_t s = nullptr;
+        if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaMalloc(&d, bytes * (size_t)(world + 1)) != cudaSuccess) {
+            err = "share_bytes: allocation failed";
+            if (s) cudaStreamDestroy(s);
+            return 1;
+        }
+        int rc = 0;
+        if (cudaMemcpyAsync(d + bytes * (size_t)world, mine, bytes, cudaMemcpyHostToDevice, s) != cudaSuccess)
+            rc = 1;
+        if (!rc) rc = check(api->AllGather(d + bytes * (size_t)world, d, bytes, ncclUint8, comm, s),
+                            "ncclAllGather(bytes)");
+        if (!rc && (cudaMemcpyAsync(all, d, bytes * (size_t)world, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+                    cudaStreamSynchronize(s) != cudaSuccess)) {
+            err = "share_bytes: copy failed";
+            rc = 1;
+        }
+        cudaFree(d);
+        cudaStreamDestroy(s);
+        return rc;
+    }
+    bool same_process() const override { return false; }
 };
 
 // ------------------------------------------------------------------------------- local
@@ -141,6 +170,7 @@ struct LocalGroup {
     std::vector<const double*> src;   // per-rank source pointer of the current collective
     std::vector<int> dev;
     std::vector<cudaEvent_t> ready, done;
+    std::vector<char> shared;                 // share_bytes staging (host)
 
     // Returns false if a rank gave up (timeout / error): every waiter then fails too.
     bool barrier(double timeout_s = 120.0) {
@@ -212,6 +242,21 @@ struct LocalTransport : Transport {
         return exchange(send, recv, (size_t)slots, true, true, s);
     }
     const char* kind() const override { return "local"; }
+    int share_bytes(const void* mine, void* all, size_t bytes) override {
+        {
+            std::lock_guard<std::mutex> lk(g->mu);
+            if (g->shared.size() < bytes * (size_t)world) g->shared.resize(bytes * (size_t)world);
+            std::memcpy(g->shared.data() + bytes * (size_t)rank, mine, bytes);
+        }
+        if (!g->barrier()) return fail_msg("local group barrier timed out or a rank failed");
+        {
+            std::lock_guard<std::mutex> lk(g->mu);
+            std::memcpy(all, g->shared.data(), bytes * (size_t)world);
+        }
+        if (!g->barrier()) return fail_msg("local group barrier timed out or a rank failed");
+        return 0;
+    }
+    bool same_process() const override { return true; }
 };
 
 }  // namespace mcr

@@ -102,7 +102,22 @@ struct Vecs {
     double* x_jac0;      // Jacobi double buffer (for sweep parity); full length when sharded
     double* x_jac1;
     long long roff;      // first global row of this shard (0 on one GPU): own slice of x_jac*
+    // Fused exchange (row shards in peer-to-peer mode): peers[slot * world + q] is rank q's
+    // copy of full vector `slot` (FV_X, FV_X1, FV_P, FV_S), mapped into this device's address
+    // space; the producer of an own-row value also stores it into every peer's copy, so the
+    // "allgather" rides NVLink while the kernel computes. Null when not in that mode.
+    double* const* peers;
+    int world, rank;
+    int xnext_slot;      // FV_X / FV_X1: which Jacobi buffer this sweep writes (set per launch)
 };
+enum FullVec : int { FV_X = 0, FV_X1 = 1, FV_P = 2, FV_S = 3 };
+
+// Store an own-row value of full vector `slot` (global index g) into every peer's copy.
+__device__ __forceinline__ void peer_store(const Vecs& V, int slot, long long g, double v) {
+    if (!V.peers) return;
+    for (int q = 0; q < V.world; ++q)
+        if (q != V.rank) V.peers[slot * V.world + q][g] = v;
+}
 
 enum Epi : int { EPI_Y = 0, EPI_RESID = 1, EPI_JACOBI = 2, EPI_S0 = 3, EPI_V = 4, EPI_T = 5 };
 enum Phase : int { PH_A = 0, PH_C = 1, PH_E = 2 };
@@ -370,6 +385,7 @@ __device__ __forceinline__ void epi_store(const Vecs& V, int row, double s, cons
     } else if constexpr (EPI == EPI_JACOBI) {
         const double xn = ddiv(dsub(in.a, s), in.b);          // (b - R x) / d
         V.xnext[row] = xn;
+        peer_store(V, V.xnext_slot, V.roff + row, xn);
         mb = umax(mb, absbits(dsub(xn, in.c)));               // |x' - x|
     } else if constexpr (EPI == EPI_S0) {
         const double r = dsub(in.a, dmul(1.0, s));            // r = b - 1.0 * (M x)
@@ -451,6 +467,7 @@ __device__ __forceinline__ const double* jacobi_select(const double* x, Vecs& V,
         const double* cur = (it & 1) ? V.x_jac0 : V.x_jac1;
         V.xcur = cur + V.roff;          // own rows (the whole vector on one GPU)
         V.xnext = ((it & 1) ? V.x_jac1 : V.x_jac0) + V.roff;
+        V.xnext_slot = (it & 1) ? FV_X1 : FV_X;
         return cur;                     // gathers read the full (allgathered) iterate
     }
     return x;
@@ -638,6 +655,9 @@ __global__ void __launch_bounds__(SP_THREADS, MCR_SP_MINB) k_spmv(Csr A, const d
                 if (tid == 0) V.P2[blockIdx.x] = acc2;
             }
         }
+    }
+    if constexpr (EPI == EPI_JACOBI) {
+        if (V.peers) __threadfence_system();  // peer stores performed before the grid retires
     }
     kernel_finish<SP_THREADS, EPI, true>(V, st, G, mb, s_red, s_redu, &s_flag);
 }
@@ -1050,8 +1070,13 @@ __global__ void __launch_bounds__(CHUNK_NT) k_phase(Vecs V, int n, SolveState* s
 #pragma unroll
         for (int u = 0; u < CHUNK_PER; ++u) {
             const int i = base + u * CHUNK_NT;
-            if (i < n) V.p[i] = dadd(r[u], dmul(beta, dsub(p[u], dmul(w, v[u]))));  // r + beta (p - w v)
+            if (i < n) {
+                const double pn = dadd(r[u], dmul(beta, dsub(p[u], dmul(w, v[u]))));  // r + beta (p - w v)
+                V.p[i] = pn;
+                peer_store(V, FV_P, V.roff + i, pn);
+            }
         }
+        if (V.peers) __threadfence_system();
     } else if constexpr (PH == PH_C) {
         const double a = st->a;
         const int stop = st->stop;
@@ -1068,9 +1093,11 @@ __global__ void __launch_bounds__(CHUNK_NT) k_phase(Vecs V, int n, SolveState* s
             if (i < n) {
                 const double sv = dsub(r[u], dmul(a, v[u]));   // s = r - a v
                 V.s[i] = sv;
+                peer_store(V, FV_S, V.roff + i, sv);
                 mb = umax(mb, absbits(sv));
             }
         }
+        if (V.peers) __threadfence_system();
         mb = group_max<CHUNK_NT / 32, 0>(mb, s_redu);
         if (threadIdx.x == 0 && mb && !stop) atomicMax(&st->maxbits, mb);
     } else {

@@ -104,6 +104,12 @@ struct mcr_matrix {
     int64_t n_global = 0, roff = 0, chunk = 0;
     std::shared_ptr<Transport> comm;
     double* recv = nullptr;           // world * SEND_SLOTS exchanged partials
+    // peer-to-peer mode (mcr_shard_enable_p2p): the full vectors live in `fullblk` (cudaMalloc,
+    // IPC-exportable); d_peers[slot * world + q] = rank q's copy, mapped here
+    int p2p = 0;
+    double* fullblk = nullptr;
+    double** d_peers = nullptr;
+    std::vector<void*> ipc_opened;
     int storage = MCR_STORAGE_CSR;
     cudaStream_t own_stream = nullptr, stream = nullptr;
     // full matrix, CSR
@@ -155,6 +161,7 @@ struct mcr_matrix {
 
     int64_t n_full() const { return comm ? chunk * world : n; }
     double* vec(int k) const {
+        if (k < V_FULL_COUNT && fullblk) return fullblk + (size_t)k * (size_t)n_full();
         return k < V_FULL_COUNT ? work + (size_t)k * (size_t)n_full()
                                 : work + (size_t)V_FULL_COUNT * (size_t)n_full() +
                                       (size_t)(k - V_FULL_COUNT) * (size_t)n;
@@ -231,6 +238,10 @@ Vecs base_vecs(const mcr_matrix* h) {
     V.x_jac0 = h->vec(V_X);
     V.x_jac1 = h->vec(V_X1);
     V.roff = h->roff;
+    V.peers = h->p2p ? h->d_peers : nullptr;
+    V.world = h->world;
+    V.rank = h->rank;
+    V.xnext_slot = FV_X;
     return V;
 }
 
@@ -429,6 +440,16 @@ int allgather_full(mcr_matrix* h, double* buf) {
     return MCR_OK;
 }
 
+// Peer-to-peer mode: the producers already stored their rows into every peer's copy; a slot
+// exchange orders those stores before any rank's next gather (every rank's producer kernel
+// has retired -- with a system-scope fence -- before it enters the exchange).
+int p2p_barrier(mcr_matrix* h) {
+    Transport& T = *h->comm;
+    if (T.gather_slots(h->st->send, h->recv, SEND_SLOTS, h->stream))
+        return fail(MCR_CUDA_ERROR, std::string(T.kind()) + " barrier: " + T.err);
+    return MCR_OK;
+}
+
 // max|b - M x| into st->resid; x is the full (gathered) vector.
 int residual_into_state(mcr_matrix* h, const double* x, int64_t* launches) {
     Vecs V = base_vecs(h);
@@ -513,8 +534,8 @@ int jacobi_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double tol
             launch_mv<EPI_JACOBI>(h, true, nullptr, V, &launched);
             if (h->sharded()) {  // sweep s writes buffer s & 1: gather it with the partial max
                 const int64_t sweep = sweeps + i + 1;
-                TRY(exchange_point<FIN_JACOBI>(h, (sweep & 1) ? h->vec(V_X1) : h->vec(V_X),
-                                               &launched));
+                double* wrote = (sweep & 1) ? h->vec(V_X1) : h->vec(V_X);
+                TRY(exchange_point<FIN_JACOBI>(h, h->p2p ? nullptr : wrote, &launched));
             }
         }
         CK(cudaGetLastError());
@@ -576,12 +597,12 @@ int bicgstab_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double t
         const int k = (int)std::min<int64_t>(batch, max_it - iters);
         for (int i = 0; i < k; ++i) {
             launch_phase<PH_A>(h, V, &launched);               // p = r + beta (p - w v)
-            if (sh) TRY(allgather_full(h, p_full));
+            if (sh) TRY(h->p2p ? p2p_barrier(h) : allgather_full(h, p_full));
             launch_mv<EPI_V>(h, false, p_full, V, &launched);  // v = M p, q.v -> a
             launch_seqdot<SQ_V>(h, V, &launched);
             if (sh) TRY(exchange_point<FIN_V>(h, nullptr, &launched));
             launch_phase<PH_C>(h, V, &launched);               // s = r - a v, max|s|
-            if (sh) TRY(allgather_full(h, s_full));
+            if (sh) TRY(h->p2p ? p2p_barrier(h) : allgather_full(h, s_full));
             launch_mv<EPI_T>(h, false, s_full, V, &launched);  // t = M s, t.t, t.s -> w
             launch_seqdot<SQ_T>(h, V, &launched);
             if (sh) TRY(exchange_point<FIN_T>(h, nullptr, &launched));
@@ -683,6 +704,9 @@ MCR_API void mcr_matrix_destroy(mcr_matrix* h) {
                 if (p) cudaFreeAsync(p, s);
             cudaStreamSynchronize(s);
         }
+        for (void* p : h->ipc_opened) cudaIpcCloseMemHandle(p);
+        if (h->fullblk) cudaFree(h->fullblk);
+        if (h->d_peers) cudaFree(h->d_peers);
         if (h->ev0) cudaEventDestroy(h->ev0);
         if (h->ev1) cudaEventDestroy(h->ev1);
         if (s) cudaStreamDestroy(s);
@@ -1076,6 +1100,60 @@ MCR_API int mcr_shard_create(mcr_comm* comm, int64_t n_global, int64_t row0, int
     const int64_t chunk = (n_global + T.world - 1) / T.world;
     return create_handle(rows, rstart, col, nonzero, T.device, MCR_STORAGE_TILES_STREAM, comm->t,
                          n_global, row0, chunk, out);
+}
+
+MCR_API int mcr_shard_enable_p2p(mcr_matrix* h) {
+    if (!h) return fail(MCR_INVALID_ARGUMENT, "NULL handle");
+    if (!h->sharded()) return fail(MCR_INVALID_ARGUMENT, "peer-to-peer mode needs a row shard");
+    std::lock_guard<std::mutex> lk(h->mu);
+    if (h->p2p) return MCR_OK;
+    DeviceGuard g(h->device);
+    Transport& T = *h->comm;
+    const size_t words = (size_t)V_FULL_COUNT * (size_t)h->n_full();
+    CK(cudaMalloc((void**)&h->fullblk, sizeof(double) * words));
+    CK(cudaMemset(h->fullblk, 0, sizeof(double) * words));
+    std::vector<double*> base((size_t)h->world, nullptr);
+    if (T.same_process()) {
+        std::vector<uint64_t> all((size_t)h->world);
+        const uint64_t mine = (uint64_t)(uintptr_t)h->fullblk;
+        if (T.share_bytes(&mine, all.data(), sizeof(mine)))
+            return fail(MCR_CUDA_ERROR, "p2p setup: " + T.err);
+        for (int q = 0; q < h->world; ++q) {
+            base[(size_t)q] = (double*)(uintptr_t)all[(size_t)q];
+            int dq = T.device;
+            if (auto* L = dynamic_cast<LocalTransport*>(&T)) dq = L->g->dev[(size_t)q];
+            if (dq != h->device) {  // another GPU of this process: map it
+                cudaError_t e = cudaDeviceEnablePeerAccess(dq, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+                    return fail(MCR_CUDA_ERROR, std::string("peer access: ") + cudaGetErrorString(e));
+                cudaGetLastError();
+            }
+        }
+    } else {
+        cudaIpcMemHandle_t mine;
+        CK(cudaIpcGetMemHandle(&mine, h->fullblk));
+        std::vector<cudaIpcMemHandle_t> all((size_t)h->world);
+        if (T.share_bytes(&mine, all.data(), sizeof(mine)))
+            return fail(MCR_CUDA_ERROR, "p2p setup: " + T.err);
+        for (int q = 0; q < h->world; ++q) {
+            if (q == h->rank) {
+                base[(size_t)q] = h->fullblk;
+                continue;
+            }
+            void* p = nullptr;
+            CK(cudaIpcOpenMemHandle(&p, all[(size_t)q], cudaIpcMemLazyEnablePeerAccess));
+            h->ipc_opened.push_back(p);
+            base[(size_t)q] = (double*)p;
+        }
+    }
+    std::vector<double*> table((size_t)V_FULL_COUNT * (size_t)h->world);
+    for (int slot = 0; slot < V_FULL_COUNT; ++slot)
+        for (int q = 0; q < h->world; ++q)
+            table[(size_t)slot * h->world + q] = base[(size_t)q] + (size_t)slot * (size_t)h->n_full();
+    CK(cudaMalloc((void**)&h->d_peers, sizeof(double*) * table.size()));
+    CK(cudaMemcpy(h->d_peers, table.data(), sizeof(double*) * table.size(), cudaMemcpyHostToDevice));
+    h->p2p = 1;
+    return MCR_OK;
 }
 
 MCR_API int mcr_generate(mcr_comm* comm, int device, int64_t n_global, double mean_offdiag,

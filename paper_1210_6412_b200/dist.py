@@ -168,6 +168,12 @@ class ShardMatrix:
                 float(tol), int(max_it), ctypes.c_void_p(d_x), ctypes.byref(rep))
         return rc, rep
 
+    def enable_p2p(self) -> None:
+        """Fused exchange (mcr_shard_enable_p2p): collective, before the first solve."""
+        rc = self._L.mcr_shard_enable_p2p(self._h)
+        if rc != _lib.MCR_OK:
+            _raise_native(rc)
+
     def set_stream(self, stream_ptr: int) -> None:
         self._L.mcr_set_stream(self._h, ctypes.c_void_p(stream_ptr))
 
@@ -236,7 +242,7 @@ def bicgstab_solve_sharded(shard: ShardMatrix, b_local, config: Optional[SolverC
 
 
 def solve_local_group(method: str, m, b, world: int, config: Optional[SolverConfig] = None,
-                      devices: Optional[Sequence[int]] = None):
+                      devices: Optional[Sequence[int]] = None, p2p: bool = False):
     """Solve ``m x = b`` as ``world`` row shards driven by ``world`` threads of this process.
 
     Returns ``(result, per_rank)``: the assembled SolveResult (full x, rank 0's iteration
@@ -258,6 +264,8 @@ def solve_local_group(method: str, m, b, world: int, config: Optional[SolverConf
         try:
             sh = ShardMatrix.from_matrix(comms[r], m)
             shards[r] = sh
+            if p2p:
+                sh.enable_p2p()
             out[r] = _solve_sharded(method, sh, b[sh.row0:sh.row0 + sh.n], config,
                                     raise_errors=False)
         except BaseException as e:  # surfaced below

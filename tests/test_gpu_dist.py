@@ -27,7 +27,7 @@ def mods():
     return dist, solvers
 
 
-def run(mods, method, name, world):
+def run(mods, method, name, world, p2p=False):
     dist, gs = mods
     m, b = system(name)
     if dist.shard_rows(m.n, world, world - 1)[1] < 1:
@@ -37,7 +37,7 @@ def run(mods, method, name, world):
     conf = gs.SolverConfig(tolerance=c["tolerance"], max_iterations=c["max_iterations"],
                            guess_seed=c["guess_seed"])
     try:
-        res, per = dist.solve_local_group(method, m, b, world, conf)
+        res, per = dist.solve_local_group(method, m, b, world, conf, p2p=p2p)
         return exp, "ok", res, None, per
     except gs.NotConverged as err:
         return exp, "not_converged", err.result, err, None
@@ -52,8 +52,8 @@ def rel_err(x, ref):
     return float(np.max(np.abs(x - ref))) / scale if len(ref) else 0.0
 
 
-def check(mods, method, name, world, iter_slack=1):
-    exp, outcome, res, err, per = run(mods, method, name, world)
+def check(mods, method, name, world, iter_slack=1, p2p=False):
+    exp, outcome, res, err, per = run(mods, method, name, world, p2p)
     assert outcome == exp["outcome"], (name, world, outcome, exp["outcome"])
     if outcome == "zero_diagonal":
         assert err.index == exp["zero_index"]
@@ -164,3 +164,35 @@ def test_nccl_transport_world_one(mods):
         comm.close()
     finally:
         tdist.destroy_process_group()
+
+
+P2P_CASES = ["c1_seed77", "c4_2000_3999", "chain_random2", "crit3_1281", "seeded_guess",
+             "grid_50_3", "kat_breakdown_qv", "kat_divergent"]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("name", P2P_CASES)
+@pytest.mark.parametrize("method", ["jacobi", "bicgstab"])
+def test_fused_p2p_exchange(mods, name, world, method):
+    """mcr_shard_enable_p2p: the producers store their rows straight into every peer's copy
+    of x / p / s; the per-sweep collective is only the slot exchange. Same bar."""
+    check(mods, method, name, world, p2p=True)
+
+
+def test_fused_p2p_bit_identical_to_allgather(mods):
+    """Fused and allgather exchange give the same bits (BiCGStab included: the exchange only
+    moves data, the arithmetic and its order are unchanged)."""
+    dist, gs = mods
+    m, b = system("c4_7647_15293")
+    for method in ("jacobi", "bicgstab"):
+        r1, _ = dist.solve_local_group(method, m, b, 3)
+        r2, _ = dist.solve_local_group(method, m, b, 3, p2p=True)
+        assert r1.iterations == r2.iterations
+        assert np.array_equal(r1.x, r2.x)
+        assert float(r1.residual_inf).hex() == float(r2.residual_inf).hex()
+
+
+@pytest.mark.slow
+def test_fused_p2p_c2(mods):
+    check(mods, "jacobi", "c2_trial0", 4, p2p=True)
+    check(mods, "bicgstab", "c2_trial0", 4, iter_slack=6, p2p=True)
