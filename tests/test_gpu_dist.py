@@ -161,6 +161,12 @@ def test_nccl_transport_world_one(mods):
         assert abs(rb.iterations - expb["iterations"]) <= 1
         assert rel_err(rb.x, expb["x"]) <= REL_TOL
         sh.close()
+        # fused-exchange setup over NCCL (IPC export + byte allgather; no peer at world 1)
+        sh = dist.ShardMatrix.from_matrix(comm, m)
+        sh.enable_p2p()
+        r2 = dist.jacobi_solve_sharded(sh, b)
+        assert r2.iterations == exp["iterations"] and sha(r2.x) == exp["x_sha256"]
+        sh.close()
         comm.close()
     finally:
         tdist.destroy_process_group()
