@@ -1367,6 +1367,18 @@ __global__ void k_col64to32(const long long* __restrict__ in, int* __restrict__ 
     }
 }
 
+// Rows must be sorted by column without duplicates (the reference's CsrMatrix invariant,
+// sparse.py:101-118): the row sums are defined in that order.
+__global__ void k_check_rows(const long long* __restrict__ rp, const int* __restrict__ col, int n,
+                             int* bad) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        for (long long e = rp[i] + 1; e < rp[i + 1]; ++e)
+            if (col[e] <= col[e - 1]) {
+                atomicExch(bad, 1);
+                break;
+            }
+}
+
 // Stored diagonal per row (0.0 if absent; rows sorted -> binary search), the off-diagonal
 // row length, and the first row whose diagonal is 0 (ZeroDiagonal). Row i of the handle is
 // global row roff + i (row shards keep global column indices).

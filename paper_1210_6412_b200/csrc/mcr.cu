@@ -767,22 +767,26 @@ static int create_impl(mcr_matrix* h, int64_t n, const int64_t* rs, const int64_
         int* bad = nullptr;
         CK(cudaMallocAsync((void**)&tmp, sizeof(long long) * (size_t)std::max<int64_t>(nnz, 1),
                            h->stream));
-        CK(cudaMallocAsync((void**)&bad, sizeof(int), h->stream));
-        CK(cudaMemsetAsync(bad, 0, sizeof(int), h->stream));
+        CK(cudaMallocAsync((void**)&bad, 2 * sizeof(int), h->stream));
+        CK(cudaMemsetAsync(bad, 0, 2 * sizeof(int), h->stream));
         CK(cudaMemcpyAsync(tmp, col, sizeof(long long) * (size_t)nnz, cudaMemcpyHostToDevice,
                            h->stream));
-        if (nnz > 0)
+        if (nnz > 0) {
             k_col64to32<<<(int)std::min<int64_t>((nnz + 255) / 256, 1 << 16), 256, 0, h->stream>>>(
                 tmp, h->col, nnz, (int)h->n_global, bad);
+            k_check_rows<<<(int)std::min<int64_t>((n + 255) / 256, 1 << 16), 256, 0, h->stream>>>(
+                h->rp, h->col, (int)n, bad + 1);
+        }
         CK(cudaGetLastError());
-        int hbad = 0;
-        CK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+        int hbad[2] = {0, 0};
+        CK(cudaMemcpyAsync(hbad, bad, 2 * sizeof(int), cudaMemcpyDeviceToHost, h->stream));
         CK(cudaFreeAsync(tmp, h->stream));
         CK(cudaFreeAsync(bad, h->stream));
         // the row tiles are cut on the host while the copies are in flight
         std::vector<int> tiles = make_tiles(n, rs, &h->max_row);
         CK(cudaStreamSynchronize(h->stream));
-        if (hbad) return fail(MCR_DIMENSION, "column index out of range");
+        if (hbad[0]) return fail(MCR_DIMENSION, "column index out of range");
+        if (hbad[1]) return fail(MCR_DIMENSION, "rows must be sorted by column without duplicates");
         return finish_create(h, n, rs, storage, &tiles);
     }
 }

@@ -200,6 +200,18 @@ def test_dimension_mismatch_and_config(gs):
         gs.SolverConfig(tolerance=0.0)
 
 
+def test_malformed_csr_rejected(gs):
+    """Upload validates the CsrMatrix invariants the row sums depend on (sparse.py:101-118)."""
+    from paper_1210_6412_b200.sparse import CsrMatrix, DimensionMismatch
+    rs = np.array([0, 2, 3], dtype=np.int64)
+    bad_order = CsrMatrix(2, rs, np.array([1, 0, 1]), np.array([1.0, 2.0, 3.0]))
+    dup = CsrMatrix(2, rs, np.array([0, 0, 1]), np.array([1.0, 2.0, 3.0]))
+    out = CsrMatrix(2, rs, np.array([0, 2, 1]), np.array([1.0, 2.0, 3.0]))
+    for m in (bad_order, dup, out):
+        with pytest.raises(DimensionMismatch):
+            gs.DeviceMatrix(m, 0)
+
+
 def test_matvec_bitwise_random(gs):
     # T/test_sparse.py:133-142 on the device
     from oracle import oracle
