@@ -255,7 +255,7 @@ int ensure_work(mcr_matrix* h) {
         CK(cudaMemsetAsync(h->work, 0, sizeof(double) * (size_t)V_FULL_COUNT * (size_t)h->n_full(),
                            h->stream));
     h->nunits = std::max({h->ntiles, h->nchunks(), h->nslabs, h->sell.nwin * (SELL_W / SELL_CTA), 1});
-    TRY(dalloc(h, &h->P, (size_t)2 * h->nunits));
+    TRY(dalloc(h, &h->P, (size_t)4 * h->nunits));  // P1, P2 (+ 2 more slots: k_bicg_small)
     if (h->sharded()) TRY(dalloc(h, &h->recv, (size_t)h->world * SEND_SLOTS));
     return MCR_OK;
 }
@@ -578,7 +578,9 @@ int bicgstab_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double t
     if (h->small_grid > 0 && !h->seqdots) {
         CK(cudaMemsetAsync(h->maxslot, 0, 3 * sizeof(unsigned long long), h->stream));
         Csr A = csr_full(h);
-        void* args[] = {&A, &V, &h->st, &h->maxslot};
+        double* parts = h->P;
+        int pstride = h->nunits;  // four partial slots of nunits >= ntiles doubles each
+        void* args[] = {&A, &V, &h->st, &h->maxslot, &parts, &pstride};
         CK(cudaLaunchCooperativeKernel((void*)k_bicg_small, h->small_grid, SM_NT, args, 0, h->stream));
         ++launched;
         TRY(read_state(h));

@@ -1,11 +1,14 @@
 #!/bin/bash
 # Build libmcr variants (tile pipeline knobs) into build/variants/<name>/libmcr.so
+# name: b<batch>m<min blocks>s<stages>t<tile nnz>
 set -e
 cd "$(dirname "$0")/.."
 mkdir -p build/variants
-for v in "b8m4s2:-DMCR_SP_BATCH=8 -DMCR_SP_MINB=4 -DMCR_SP_STAGES=2" "b4m4s2:-DMCR_SP_BATCH=4 -DMCR_SP_MINB=4 -DMCR_SP_STAGES=2" "b8m3s2:-DMCR_SP_BATCH=8 -DMCR_SP_MINB=3 -DMCR_SP_STAGES=2" "b8m2s3:-DMCR_SP_BATCH=8 -DMCR_SP_MINB=2 -DMCR_SP_STAGES=3"; do
-  name=${v%%:*}; flags=${v#*:}
-  mkdir -p build/variants/$name
-  nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC -Xcompiler -fvisibility=hidden -shared -Iinclude $flags -o build/variants/$name/libmcr.so paper_1210_6412_b200/csrc/mcr.cu &
+for v in "$@"; do
+  b=$(echo $v | sed -E 's/b([0-9]+)m.*/\1/'); m=$(echo $v | sed -E 's/.*m([0-9]+)s.*/\1/')
+  s=$(echo $v | sed -E 's/.*s([0-9]+)t.*/\1/'); t=$(echo $v | sed -E 's/.*t([0-9]+)$/\1/')
+  mkdir -p build/variants/$v
+  nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC -Xcompiler -fvisibility=hidden -shared -Iinclude \
+    -DMCR_SP_BATCH=$b -DMCR_SP_MINB=$m -DMCR_SP_STAGES=$s -DMCR_TILE_NNZ=$t -o build/variants/$v/libmcr.so paper_1210_6412_b200/csrc/mcr.cu &
 done
 wait
