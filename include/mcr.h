@@ -43,7 +43,8 @@ enum {
     MCR_ZERO_DIAGONAL = 3,     /* ZeroDiagonal: report->zero_diagonal_index                  */
     MCR_DIMENSION = 4,         /* malformed CSR / mismatched sizes                           */
     MCR_CUDA_ERROR = 5,        /* CUDA failure; see mcr_last_error()                         */
-    MCR_INVALID_ARGUMENT = 6
+    MCR_INVALID_ARGUMENT = 6,
+    MCR_UNSUPPORTED_INPUT = 7  /* text readers: outside the fast subset (mcr_text_reason())  */
 };
 
 /* Breakdown.which of the reference (solvers.py:465-480). */
@@ -209,7 +210,8 @@ MCR_API int mcr_matrix_export(mcr_matrix* m, int64_t* rstart, int64_t* col, doub
  *                     uncertain[k], M (k+1 / m / m) and rhs[k]; any pointer may be NULL.
  *   mcr_chain_matrix  the solve-ready handle of M (owned by the chain: do not destroy).
  *   mcr_chain_solve   method 0 Jacobi / 1 BiCGStab (dots 1 = reference-order inner products)
- *                     on M x = rhs; on success x_out[n] = 1 on prob-one states, 0 on prob-zero
+ *                     on M x = rhs from x0[k] (NULL: zeros); on success x_out[n] = 1 on
+ *                     prob-one states, 0 on prob-zero
  *                     states, clip(x, 0, 1) on the uncertain ones. xs_out[k] receives the
  *                     reduced solution (also on NotConverged / Breakdown). Status as mcr_jacobi.
  * ------------------------------------------------------------------------------------- */
@@ -224,8 +226,30 @@ MCR_API int mcr_chain_export(mcr_chain* chain, int8_t* classes, int64_t* uncerta
                              int64_t* m_rstart, int64_t* m_col, double* m_nonzero, double* rhs);
 MCR_API int mcr_chain_matrix(mcr_chain* chain, mcr_matrix** out);
 MCR_API int mcr_chain_solve(mcr_chain* chain, int method, int dots, double tol,
-                            int64_t max_iterations, double* x_out, double* xs_out,
-                            mcr_report* report);
+                            int64_t max_iterations, const double* x0, double* x_out,
+                            double* xs_out, mcr_report* report);
+
+/* ---------------------------------------------------------------------------------------
+ * Text formats (formats.py read_matrix / read_vector / read_dtmc):
+ * multithreaded readers (threads <= 0: all cores) returning the reference's result --
+ * matrices in csr_from_triplets order with explicit zeros dropped, chains validated as by
+ * validate(), values parsed exactly like Python's float(). Files outside the well-formed
+ * plain-decimal subset (any error, duplicate, failed check, inf/nan, underscores, non-ASCII)
+ * return MCR_UNSUPPORTED_INPUT; mcr_text_reason() says why and the caller defers to the
+ * reference reader for its exact error. Results: mcr_text_info (n, stored entries m, initial
+ * state, goal count) then mcr_text_export (rstart[n+1], col[m], values[m] -- or values[n] of a
+ * vector -- and sorted unique goals[ngoals]).
+ * ------------------------------------------------------------------------------------- */
+typedef struct mcr_text mcr_text;
+MCR_API int mcr_read_matrix(const char* path, int threads, mcr_text** out);
+MCR_API int mcr_read_vector(const char* path, int threads, mcr_text** out);
+MCR_API int mcr_read_dtmc(const char* path, int threads, mcr_text** out);
+MCR_API int mcr_text_info(const mcr_text* text, int64_t* n, int64_t* m, int64_t* initial,
+                          int64_t* ngoals);
+MCR_API int mcr_text_export(const mcr_text* text, int64_t* rstart, int64_t* col, double* values,
+                            int64_t* goals);
+MCR_API void mcr_text_destroy(mcr_text* text);
+MCR_API const char* mcr_text_reason(void);
 
 /* Message of the last failing call on this thread ("" if none). */
 MCR_API const char* mcr_last_error(void);

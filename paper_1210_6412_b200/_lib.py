@@ -32,8 +32,10 @@ EXPORTS = (
     "mcr_comm_destroy", "mcr_comm_info", "mcr_shard_create", "mcr_generate",
     "mcr_generate_rhs", "mcr_matrix_export", "mcr_chain_create", "mcr_chain_destroy",
     "mcr_chain_info", "mcr_chain_export", "mcr_chain_matrix", "mcr_chain_solve",
-    "mcr_shard_enable_p2p",
+    "mcr_shard_enable_p2p", "mcr_read_matrix", "mcr_read_vector", "mcr_read_dtmc",
+    "mcr_text_info", "mcr_text_export", "mcr_text_destroy", "mcr_text_reason",
 )
+MCR_UNSUPPORTED_INPUT = 7
 COMM_ID_BYTES = 128
 DOTS_TREE, DOTS_SEQUENTIAL = 0, 1
 
@@ -119,13 +121,21 @@ def load():
     L.mcr_generate_rhs.argtypes = [vp, ctypes.c_uint64, vp]
     L.mcr_matrix_export.argtypes = [vp, vp, vp, vp]
     L.mcr_shard_enable_p2p.argtypes = [vp]
+    for name in ("mcr_read_matrix", "mcr_read_vector", "mcr_read_dtmc"):
+        getattr(L, name).argtypes = [ctypes.c_char_p, ip, ctypes.POINTER(vp)]
+    L.mcr_text_info.argtypes = [vp, pi64, pi64, pi64, pi64]
+    L.mcr_text_export.argtypes = [vp, vp, vp, vp, vp]
+    L.mcr_text_destroy.argtypes = [vp]
+    L.mcr_text_destroy.restype = None
+    L.mcr_text_reason.restype = ctypes.c_char_p
+    L.mcr_text_reason.argtypes = []
     L.mcr_chain_create.argtypes = [i64, vp, vp, vp, vp, i64, ip, ctypes.POINTER(vp)]
     L.mcr_chain_destroy.argtypes = [vp]
     L.mcr_chain_destroy.restype = None
     L.mcr_chain_info.argtypes = [vp, pi64, pi64, pi64, pi64]
     L.mcr_chain_export.argtypes = [vp, vp, vp, vp, vp, vp, vp]
     L.mcr_chain_matrix.argtypes = [vp, ctypes.POINTER(vp)]
-    L.mcr_chain_solve.argtypes = [vp, ip, ip, dbl, i64, vp, vp, ctypes.POINTER(Report)]
+    L.mcr_chain_solve.argtypes = [vp, ip, ip, dbl, i64, vp, vp, vp, ctypes.POINTER(Report)]
     L.mcr_last_error.restype = ctypes.c_char_p
     L.mcr_last_error.argtypes = []
     _lib = L

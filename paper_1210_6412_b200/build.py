@@ -10,8 +10,10 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libmcr.so")
-SOURCES = [os.path.join(CSRC, "mcr.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, "device.cuh"), os.path.join(ROOT, "include", "mcr.h")]
+SOURCES = [os.path.join(CSRC, "mcr.cu"), os.path.join(CSRC, "formats.cpp")]
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("device.cuh", "comm.h", "generator.cuh",
+                                                  "chain.cuh")] + [
+    os.path.join(ROOT, "include", "mcr.h")]
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17",

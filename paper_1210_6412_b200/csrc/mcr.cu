@@ -1498,7 +1498,7 @@ MCR_API int mcr_chain_matrix(mcr_chain* c, mcr_matrix** out) {
 }
 
 MCR_API int mcr_chain_solve(mcr_chain* c, int method, int dots, double tol, int64_t max_it,
-                            double* x_out, double* xs_out, mcr_report* rep) {
+                            const double* x0, double* x_out, double* xs_out, mcr_report* rep) {
     if (!c || !rep) return fail(MCR_INVALID_ARGUMENT, "NULL argument");
     if (method != 0 && method != 1) return fail(MCR_INVALID_ARGUMENT, "method: 0 jacobi, 1 bicgstab");
     if (!(tol > 0.0)) return fail(MCR_INVALID_ARGUMENT, "tolerance must be positive");
@@ -1523,10 +1523,13 @@ MCR_API int mcr_chain_solve(mcr_chain* c, int method, int dots, double tol, int6
         std::lock_guard<std::mutex> lc(c->mu);
         if (!c->xs) TRY(calloc_owned(c, &c->xs, (size_t)c->k));
         if (!c->xfull) TRY(calloc_owned(c, &c->xfull, (size_t)c->n));
+        if (x0) CK(cudaMemcpyAsync(c->xfull, x0, sizeof(double) * (size_t)c->k,
+                                   cudaMemcpyHostToDevice, c->stream));  // staging
         CK(cudaStreamSynchronize(c->stream));
     }
-    const int rc = method == 0 ? jacobi_impl(M, c->rhs, nullptr, tol, max_it, c->xs, rep)
-                               : bicgstab_impl(M, c->rhs, nullptr, tol, max_it, c->xs, rep);
+    const double* d_x0 = x0 ? c->xfull : nullptr;  // consumed before xfull is rewritten
+    const int rc = method == 0 ? jacobi_impl(M, c->rhs, d_x0, tol, max_it, c->xs, rep)
+                               : bicgstab_impl(M, c->rhs, d_x0, tol, max_it, c->xs, rep);
     if (rc != MCR_OK && rc != MCR_NOT_CONVERGED && rc != MCR_BREAKDOWN) return rc;
     const std::string msg = g_err;
     if (xs_out)

@@ -129,15 +129,18 @@ class ChainSystem:
         except KeyError:
             raise ValueError(f"unknown method {method!r}, expected one of {sorted(METHODS)}") from None
         cfg = config or SolverConfig()
-        if getattr(cfg, "guess_seed", None) is not None:
-            raise ValueError("guess_seed is not supported by the device chain solve")
+        x0 = None
+        seed = getattr(cfg, "guess_seed", None)
+        if seed is not None and self.k:  # solvers.py:153-156 on the reduced system
+            x0 = np.ascontiguousarray(np.random.default_rng(seed).random(self.k))
         x = np.empty(self.n)
         xs = np.empty(self.k)
         rep = _lib.Report()
         start = time.perf_counter()
         rc = self._L.mcr_chain_solve(self._h, code, dots, float(cfg.tolerance),
-                                     int(cfg.max_iterations), x.ctypes.data, xs.ctypes.data,
-                                     ctypes.byref(rep))
+                                     int(cfg.max_iterations),
+                                     None if x0 is None else x0.ctypes.data, x.ctypes.data,
+                                     xs.ctypes.data, ctypes.byref(rep))
         if self.k == 0:  # markov.py:287-288
             return x, SolveResult(np.zeros(0), 0, True, 0.0, 0.0)
         result, err = outcome(rc, xs, rep, start)

@@ -103,3 +103,14 @@ def test_build_system_returns_reference_types(gm):
     assert isinstance(s, mm.LinearSystem) and isinstance(s.partition, mm.StatePartition)
     c = manifest()["oracle_chain_3"]
     assert sha(s.rhs) == c["rhs_sha256"] and sha(s.matrix.nonzero) == c["m_nonzero_sha256"]
+
+
+def test_seeded_guess_chain(gm):
+    """guess_seed starts the reduced solve from default_rng(seed).random(k), as the
+    reference's _initial_guess does (solvers.py:153-156)."""
+    from paper_1210_6412_b200.solvers import SolverConfig
+    ch, goals = chain("dtmc_1000")
+    x0, r0 = gm.reachability_probabilities(ch, goals, "jacobi-gpu")
+    x1, r1 = gm.reachability_probabilities(ch, goals, "jacobi-gpu", SolverConfig(guess_seed=7))
+    assert r1.converged and np.max(np.abs(x1 - x0)) <= 1e-8
+    assert r1.iterations != r0.iterations or not np.array_equal(x1, x0)
