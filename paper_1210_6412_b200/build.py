@@ -11,8 +11,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libmcr.so")
 SOURCES = [os.path.join(CSRC, "mcr.cu"), os.path.join(CSRC, "formats.cpp")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("device.cuh", "comm.h", "generator.cuh",
-                                                  "chain.cuh")] + [
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC))
+                  if f.endswith((".h", ".cuh"))] + [
     os.path.join(ROOT, "include", "mcr.h")]
 
 NVCC_FLAGS = [

@@ -1,0 +1,257 @@
+// handle.h -- host-side state of libmcr.so: error plumbing, the matrix / communicator / chain
+// handles, device allocation helpers and the work-vector layout. Part of the single
+// translation unit mcr.cu (included in order: handle.h, storage.cuh, solve.cuh, chain_host.cuh).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <cub/device/device_scan.cuh>
+
+#include "comm.h"
+#include "device.cuh"
+#include "chain.cuh"
+#include "generator.cuh"
+#include "mcr.h"
+
+using namespace mcr;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CK(call)                                                                        \
+    do {                                                                                \
+        cudaError_t e_ = (call);                                                        \
+        if (e_ != cudaSuccess)                                                          \
+            return fail(MCR_CUDA_ERROR, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+// Work vectors. FULL ones are gather inputs of the SpMV and span the whole system when the
+// matrix is a row shard (world * chunk entries, indexed by global row); the others hold this
+// handle's rows only. On one GPU both kinds are n long.
+enum { V_X = 0, V_X1, V_P, V_S, V_FULL_COUNT, V_B = V_FULL_COUNT, V_R, V_Q, V_V, V_T, V_COUNT };
+
+}  // namespace
+
+struct mcr_matrix;
+
+// A Markov chain with its goal set and the reduced system built from it (chain.cuh).
+struct mcr_chain {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int64_t n = 0, nnz = 0, k = 0, m_nnz = 0, nzero = 0, none = 0;
+    long long* rp = nullptr;
+    int* col = nullptr;
+    double* val = nullptr;
+    unsigned char* goal = nullptr;
+    signed char* cls = nullptr;
+    long long* remap = nullptr;
+    long long* list = nullptr;
+    long long* mrp = nullptr;
+    int* mcol = nullptr;
+    double* mval = nullptr;
+    double* rhs = nullptr;
+    double* xs = nullptr;
+    double* xfull = nullptr;
+    mcr_matrix* M = nullptr;  // solve-ready handle of M (created on first use)
+    std::vector<void*> owned;
+    std::mutex mu;
+};
+
+// Communicator of a row-sharded solve (comm.h): NCCL, or the in-process local group.
+struct mcr_comm {
+    std::shared_ptr<mcr::Transport> t;
+};
+
+struct mcr_matrix {
+    int device = 0;
+    int64_t n = 0, nnz = 0;           // rows (and entries) held by this handle
+    // row sharding: this handle holds rows [roff, roff + n) of an n_global system; every rank
+    // holds `chunk` = ceil(n_global / world) rows except the last
+    int world = 1, rank = 0;
+    int64_t n_global = 0, roff = 0, chunk = 0;
+    std::shared_ptr<Transport> comm;
+    double* recv = nullptr;           // world * SEND_SLOTS exchanged partials
+    // peer-to-peer mode (mcr_shard_enable_p2p): the full vectors live in `fullblk` (cudaMalloc,
+    // IPC-exportable); d_peers[slot * world + q] = rank q's copy, mapped here
+    int p2p = 0;
+    double* fullblk = nullptr;
+    double** d_peers = nullptr;
+    std::vector<void*> ipc_opened;
+    int storage = MCR_STORAGE_CSR;
+    cudaStream_t own_stream = nullptr, stream = nullptr;
+    // full matrix, CSR
+    long long* rp = nullptr;
+    int* col = nullptr;
+    double* val = nullptr;
+    int* tile_row = nullptr;
+    TileDesc* desc = nullptr;     // tiles of the full matrix
+    TileDesc* rdesc = nullptr;    // tiles of the off-diagonal copy
+    int ntiles = 0;
+    // off-diagonal copy for Jacobi (lazy)
+    long long* offlen = nullptr;
+    long long* rrp = nullptr;
+    int* rcol = nullptr;
+    double* rval = nullptr;
+    bool r_ready = false;
+    // SELL-32-sigma copies (short-row matrices): full matrix and off-diagonal R
+    struct SellDev {
+        long long* sptr = nullptr;
+        int* perm = nullptr;
+        int* col = nullptr;
+        double* val = nullptr;
+        long long* swidth = nullptr;
+        int nwin = 0;
+        long long slots = 0;
+    } sell, rsell;
+    bool use_sell = false;
+    // dense slabs
+    double* dense = nullptr;
+    int nslabs = 0;
+    // diagonal + facts
+    double* d = nullptr;
+    long long first_zero = -1;
+    long long max_row = 0;
+    // workspace
+    double* work = nullptr;
+    double* P = nullptr;
+    int nunits = 0;
+    SolveState* st = nullptr;
+    SolveState h_state{};
+    SolveState* h_st = &h_state;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    int64_t bytes = 0;
+    int seqdots = 0;
+    int spmv_grid = 1;
+    int small_grid = 0;                     // > 0: whole solve in one cooperative launch
+    unsigned long long* maxslot = nullptr;  // 3 slots for the persistent solvers
+    std::mutex mu;
+
+    int64_t n_full() const { return comm ? chunk * world : n; }
+    double* vec(int k) const {
+        if (k < V_FULL_COUNT && fullblk) return fullblk + (size_t)k * (size_t)n_full();
+        return k < V_FULL_COUNT ? work + (size_t)k * (size_t)n_full()
+                                : work + (size_t)V_FULL_COUNT * (size_t)n_full() +
+                                      (size_t)(k - V_FULL_COUNT) * (size_t)n;
+    }
+    // a row shard (mcr_shard_create) runs the exchange points even at world 1, so the NCCL
+    // transport is exercised end to end on a one-GPU box
+    bool sharded() const { return comm != nullptr; }
+    int nchunks() const { return (int)((n + CHUNK_ROWS - 1) / CHUNK_ROWS); }
+};
+
+namespace {
+
+// Device memory comes from the device's stream-ordered pool (cudaMallocAsync) with the
+// release threshold lifted, so creating and destroying handles (the end-to-end path uploads a
+// matrix per solve) recycles memory instead of paying cudaMalloc/cudaFree each time.
+template <class T>
+int dalloc(mcr_matrix* h, T** p, size_t count) {
+    *p = nullptr;
+    if (count == 0) count = 1;
+    CK(cudaMallocAsync((void**)p, sizeof(T) * count, h->stream));
+    h->bytes += (int64_t)(sizeof(T) * count);
+    return MCR_OK;
+}
+
+template <class T>
+void dfree(mcr_matrix* h, T*& p, size_t count) {
+    if (p) {
+        cudaFreeAsync(p, h->stream);
+        h->bytes -= (int64_t)(sizeof(T) * (count ? count : 1));
+        p = nullptr;
+    }
+}
+
+int keep_pool_memory(int device) {
+    static std::mutex mu;
+    static std::vector<int> done;
+    std::lock_guard<std::mutex> lk(mu);
+    if (std::find(done.begin(), done.end(), device) != done.end()) return MCR_OK;
+    cudaMemPool_t pool;
+    CK(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = UINT64_MAX;
+    CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    done.push_back(device);
+    return MCR_OK;
+}
+
+#define TRY(x)                   \
+    do {                         \
+        int rc_ = (x);           \
+        if (rc_ != MCR_OK) return rc_; \
+    } while (0)
+
+Csr csr_full(const mcr_matrix* h) {
+    return Csr{h->rp, h->col, h->val, h->desc, h->ntiles, (int)h->n};
+}
+Csr csr_off(const mcr_matrix* h) {
+    return Csr{h->rrp, h->rcol, h->rval, h->rdesc, h->ntiles, (int)h->n};
+}
+
+// Own-row views (x, p, s point at this rank's slice of the full vectors).
+Vecs base_vecs(const mcr_matrix* h) {
+    Vecs V{};
+    V.b = h->vec(V_B);
+    V.d = h->d;
+    V.x = h->vec(V_X) + h->roff;
+    V.r = h->vec(V_R);
+    V.q = h->vec(V_Q);
+    V.p = h->vec(V_P) + h->roff;
+    V.v = h->vec(V_V);
+    V.s = h->vec(V_S) + h->roff;
+    V.t = h->vec(V_T);
+    V.P1 = h->P;
+    V.P2 = h->P + h->nunits;
+    V.x_jac0 = h->vec(V_X);
+    V.x_jac1 = h->vec(V_X1);
+    V.roff = h->roff;
+    V.peers = h->p2p ? h->d_peers : nullptr;
+    V.world = h->world;
+    V.rank = h->rank;
+    V.xnext_slot = FV_X;
+    return V;
+}
+
+int ensure_work(mcr_matrix* h) {
+    if (h->work) return MCR_OK;
+    const size_t words = (size_t)V_FULL_COUNT * (size_t)h->n_full() +
+                         (size_t)(V_COUNT - V_FULL_COUNT) * (size_t)h->n;
+    TRY(dalloc(h, &h->work, words));
+    // full vectors start zeroed: blocks past the last rank's rows are gathered but never read
+    if (h->sharded())
+        CK(cudaMemsetAsync(h->work, 0, sizeof(double) * (size_t)V_FULL_COUNT * (size_t)h->n_full(),
+                           h->stream));
+    h->nunits = std::max({h->ntiles, h->nchunks(), h->nslabs, h->sell.nwin * (SELL_W / SELL_CTA), 1});
+    TRY(dalloc(h, &h->P, (size_t)4 * h->nunits));  // P1, P2 (+ 2 more slots: k_bicg_small)
+    if (h->sharded()) TRY(dalloc(h, &h->recv, (size_t)h->world * SEND_SLOTS));
+    return MCR_OK;
+}
+
+}  // namespace

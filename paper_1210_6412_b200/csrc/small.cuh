@@ -1,0 +1,292 @@
+// small.cuh -- whole-solve cooperative kernels for systems whose tiles all fit on the GPU at once (part of device.cuh).
+#pragma once
+
+#include "common.cuh"
+
+namespace mcr {
+
+// ---------------------------------------------------------------- persistent small-system solvers
+// For systems whose tiles all fit on the GPU at once (ntiles <= co-resident CTAs, e.g. C1 and
+// the Table-1 shapes) one cooperative kernel runs the whole solve: sweeps / iterations are
+// separated by grid barriers instead of kernel launches, and every CTA reduces the per-tile
+// partials itself in the same fixed order, so all CTAs hold bit-identical scalars without a
+// round trip through global state.
+namespace cg = cooperative_groups;
+constexpr int SM_NT = TILE_ROWS;
+
+struct SmallSmem {
+    double val[TILE_NNZ];      // this CTA's tile, loaded once per solve
+    int col[TILE_NNZ];
+    double prod[TILE_NNZ];
+    int rp[TILE_ROWS + 1];
+    double red[SM_NT / 32];
+    unsigned long long redu[SM_NT / 32];
+    long long e0, e1;
+    int nrows, r0, cached;
+};
+
+// One tile per CTA (grid == ntiles): its row pointers, columns and values move to shared
+// memory once per solve; a single row longer than a tile stays in HBM and is streamed.
+__device__ __forceinline__ void load_tile(const Csr& A, int t, SmallSmem& sm) {
+    if (threadIdx.x == 0) {
+        const TileDesc d = A.desc[t];
+        sm.e0 = d.e0;
+        sm.e1 = d.e1;
+        sm.nrows = d.r1 - d.r0;
+        sm.r0 = d.r0;
+        sm.cached = (d.e1 - d.e0) <= TILE_NNZ;
+    }
+    __syncthreads();
+    if (sm.cached) {
+        const int len = (int)(sm.e1 - sm.e0);
+        for (int k = threadIdx.x; k < len; k += SM_NT) {
+            sm.val[k] = A.val[sm.e0 + k];
+            sm.col[k] = A.col[sm.e0 + k];
+        }
+        for (int k = threadIdx.x; k <= sm.nrows; k += SM_NT)
+            sm.rp[k] = (int)(A.rp[sm.r0 + k] - sm.e0);
+    }
+    __syncthreads();
+}
+
+// Row sums of the CTA's tile against x_j = G(j): products (one rounding each) for all entries
+// at once, then thread r adds its row left to right. G uses plain (L1-cached) loads: within a
+// phase the gathered vectors are read-only, and the grid barrier between phases is a
+// gpu-scope fence, which invalidates L1 (so the next phase never sees a stale line).
+template <class Gather>
+__device__ __forceinline__ double tile_rowsum(const Csr& A, SmallSmem& sm, Gather G) {
+    const int tid = threadIdx.x;
+    double acc = 0.0;
+    if (sm.cached) {
+        const int len = (int)(sm.e1 - sm.e0);
+        for (int k = tid; k < len; k += SM_NT) sm.prod[k] = dmul(sm.val[k], G(sm.col[k]));
+        __syncthreads();
+        if (tid < sm.nrows) {
+            const int b = sm.rp[tid], e = sm.rp[tid + 1];
+            for (int k = b; k < e; ++k) acc = dadd(acc, sm.prod[k]);
+        }
+        __syncthreads();
+    } else {  // one long row
+        double a = 0.0;
+        for (long long b0 = sm.e0; b0 < sm.e1; b0 += TILE_NNZ) {
+            const int clen = (int)((sm.e1 - b0) < TILE_NNZ ? (sm.e1 - b0) : TILE_NNZ);
+            for (int k = tid; k < clen; k += SM_NT)
+                sm.prod[k] = dmul(A.val[b0 + k], G(A.col[b0 + k]));
+            __syncthreads();
+            if (tid == 0)
+                for (int k = 0; k < clen; ++k) a = dadd(a, sm.prod[k]);
+            __syncthreads();
+        }
+        acc = a;
+    }
+    return acc;
+}
+
+// Same fixed-order reduction as reduce_partials, run by every CTA (L2 reads: the partials
+// were just written by other CTAs).
+__device__ __forceinline__ double all_reduce_partials(const double* P, int count, double* red) {
+    double acc = 0.0;
+    for (int k = threadIdx.x; k < count; k += SM_NT) acc = dadd(acc, __ldcg(P + k));
+    acc = group_sum<SM_NT / 32, 0>(acc, red);
+    if (threadIdx.x == 0) red[0] = acc;
+    __syncthreads();
+    acc = red[0];
+    __syncthreads();
+    return acc;
+}
+
+__device__ __forceinline__ double read_max(unsigned long long* slot) {
+    return bits2d(__ldcg(slot));
+}
+
+// Jacobi, all sweeps in one launch. maxslot[3] are zero on entry. Each thread keeps its row's
+// b, d and current iterate in registers; per sweep only the gathers, the x' store and one
+// grid barrier remain.
+__global__ void __launch_bounds__(SM_NT) k_jacobi_small(Csr R, Vecs V, SolveState* st,
+                                                        unsigned long long* maxslot) {
+    __shared__ SmallSmem sm;
+    cg::grid_group grid = cg::this_grid();
+    const double tol = st->tol;
+    const long long max_it = st->max_it;
+    load_tile(R, blockIdx.x, sm);
+    const int row = threadIdx.x < sm.nrows ? sm.r0 + (int)threadIdx.x : -1;
+    double bi = 0.0, di = 1.0, xi = 0.0;
+    if (row >= 0) { bi = V.b[row]; di = V.d[row]; xi = V.x_jac0[row]; }
+    long long it = 0;
+    int stop = RUNNING;
+    while (stop == RUNNING) {
+        ++it;
+        const double* xin = (it & 1) ? V.x_jac0 : V.x_jac1;
+        double* xout = (it & 1) ? V.x_jac1 : V.x_jac0;
+        const double s = tile_rowsum(R, sm, [&](int c) { return xin[c]; });
+        unsigned long long mb = 0;
+        if (row >= 0) {
+            const double xn = ddiv(dsub(bi, s), di);   // (b - R x) / d
+            xout[row] = xn;
+            mb = absbits(dsub(xn, xi));
+            xi = xn;
+        }
+        mb = group_max<SM_NT / 32, 0>(mb, sm.redu);
+        if (threadIdx.x == 0 && mb) atomicMax(&maxslot[it % 3], mb);
+        // slot (it+1)%3 was last read before the previous barrier by every CTA: clear it for
+        // the next sweep before this barrier, so no CTA can add to it before it is cleared
+        if (blockIdx.x == 0 && threadIdx.x == 0) maxslot[(it + 1) % 3] = 0ull;
+        grid.sync();
+        const double md = read_max(&maxslot[it % 3]);
+        if (md <= tol) stop = CONVERGED;
+        else if (it >= max_it) stop = NOTCONV;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        st->it = it;
+        st->stop = stop;
+    }
+}
+
+// BiCGStab, whole solve in one launch (solvers.py:450-491), three grid barriers per iteration.
+// Each thread keeps its row's r, p, v, x, q in registers. The vectors other CTAs gather are
+// recomputed on the fly from global copies instead of being materialised by extra phases:
+//   v = M p   gathers p_j = r_j + beta (p_j - w v_j) from r, p_prev, v_prev (phase A fused),
+//   t = M s   gathers s_j = r_j - a v_j from r, v (phase C fused),
+// with exactly the reference's expressions, so every value is bit-identical to the phased
+// kernels. p and v are double-buffered by iteration parity (V.p/V.s, V.v/V.t): other CTAs
+// still read the previous pair while this iteration's is written. Partials live in four
+// separate slots (parts + k*pstride: q.v, t.t, t.s, q.r) because no barrier separates a
+// slot's all-reduce from the next slot's writes. maxslot[2] zero on entry.
+__global__ void __launch_bounds__(SM_NT) k_bicg_small(Csr A, Vecs V, SolveState* st,
+                                                      unsigned long long* maxslot, double* parts,
+                                                      int pstride) {
+    __shared__ SmallSmem sm;
+    cg::grid_group grid = cg::this_grid();
+    const double tol = st->tol;
+    const long long max_it = st->max_it;
+    const int nt = A.ntiles;
+    double* Pqv = parts;
+    double* Ptt = parts + pstride;
+    double* Pts = parts + 2 * pstride;
+    double* Pqr = parts + 3 * pstride;
+    double* Rg = V.r;
+    load_tile(A, blockIdx.x, sm);
+    const int tid = threadIdx.x;
+    const int row = tid < sm.nrows ? sm.r0 + tid : -1;
+    double xi = 0.0, bi = 0.0;
+    if (row >= 0) { xi = V.x[row]; bi = V.b[row]; }
+    // setup: r = b - 1.0 * M x0, q = r, p = v = 0
+    const double* X = V.x;
+    const double s0 = tile_rowsum(A, sm, [&](int c) { return X[c]; });
+    double ri = 0.0, qi = 0.0, pi = 0.0, vi = 0.0;
+    unsigned long long mb = 0;
+    double p1 = 0.0;
+    if (row >= 0) {
+        ri = dsub(bi, dmul(1.0, s0));
+        qi = ri;
+        Rg[row] = ri;
+        V.p[row] = 0.0;  // buffer 0 of the (p, v) pair read by iteration 1
+        V.v[row] = 0.0;
+        mb = absbits(ri);
+        p1 = dmul(ri, ri);
+    }
+    p1 = group_sum<SM_NT / 32, 0>(p1, sm.red);
+    if (tid == 0) Pqr[blockIdx.x] = p1;
+    mb = group_max<SM_NT / 32, 0>(mb, sm.redu);
+    if (tid == 0 && mb) atomicMax(&maxslot[0], mb);
+    grid.sync();
+    int stop = RUNNING, which = 0;
+    long long it = 0, bd_it = 0;
+    double y = 1.0, a = 1.0, w = 1.0, beta = 0.0;
+    {
+        const double mr = read_max(&maxslot[0]);
+        const double qr = all_reduce_partials(Pqr, nt, sm.red);
+        if (mr <= tol) {
+            stop = CONVERGED;
+        } else {
+            const double denom = dmul(y, w);
+            y = qr;
+            if (tiny(denom)) { stop = BREAKDOWN; which = 1; bd_it = 1; }
+            else beta = ddiv(dmul(qr, a), denom);
+        }
+    }
+    while (stop == RUNNING) {
+        const long long cur = it + 1;
+        const bool odd = (cur & 1) != 0;          // odd iterations read pair 0, write pair 1
+        const double* Pold = odd ? V.p : V.s;
+        const double* Vold = odd ? V.v : V.t;
+        double* Pnew = odd ? V.s : V.p;
+        double* Vnew = odd ? V.t : V.v;
+        // v = M p with p = r + beta (p - w v) formed at each gathered column
+        const double sv = tile_rowsum(A, sm, [&](int c) {
+            return dadd(Rg[c], dmul(beta, dsub(Pold[c], dmul(w, Vold[c]))));
+        });
+        p1 = 0.0;
+        if (row >= 0) {
+            pi = dadd(ri, dmul(beta, dsub(pi, dmul(w, vi))));
+            vi = sv;
+            Pnew[row] = pi;
+            Vnew[row] = vi;
+            p1 = dmul(qi, vi);
+        }
+        p1 = group_sum<SM_NT / 32, 0>(p1, sm.red);
+        if (tid == 0) Pqv[blockIdx.x] = p1;
+        if (blockIdx.x == 0 && tid == 0) maxslot[1] = 0ull;
+        grid.sync();
+        const double qv = all_reduce_partials(Pqv, nt, sm.red);
+        if (tiny(qv)) { stop = BREAKDOWN; which = 2; bd_it = cur; break; }
+        a = ddiv(y, qv);
+        // t = M s with s = r - a v formed at each gathered column; s, max|s| for own rows
+        const double st_ = tile_rowsum(A, sm, [&](int c) {
+            return dsub(Rg[c], dmul(a, Vnew[c]));
+        });
+        double si = 0.0, ti = 0.0, p2 = 0.0;
+        p1 = 0.0;
+        mb = 0;
+        if (row >= 0) {
+            si = dsub(ri, dmul(a, vi));
+            ti = st_;
+            mb = absbits(si);
+            p1 = dmul(ti, ti);
+            p2 = dmul(ti, si);
+        }
+        mb = group_max<SM_NT / 32, 0>(mb, sm.redu);
+        if (tid == 0 && mb) atomicMax(&maxslot[1], mb);
+        p1 = group_sum<SM_NT / 32, 0>(p1, sm.red);
+        p2 = group_sum<SM_NT / 32, 0>(p2, sm.red);
+        if (tid == 0) { Ptt[blockIdx.x] = p1; Pts[blockIdx.x] = p2; }
+        grid.sync();
+        const bool small = read_max(&maxslot[1]) <= tol;
+        const double tt = all_reduce_partials(Ptt, nt, sm.red);
+        const double ts = all_reduce_partials(Pts, nt, sm.red);
+        if (tiny(tt)) {
+            if (!small) { stop = BREAKDOWN; which = 3; bd_it = cur; break; }
+            w = 0.0;
+        } else {
+            w = ddiv(ts, tt);
+        }
+        // x += a p + w s, r = s - w t, q.r
+        p1 = 0.0;
+        if (row >= 0) {
+            xi = dadd(dadd(xi, dmul(a, pi)), dmul(w, si));
+            ri = dsub(si, dmul(w, ti));
+            Rg[row] = ri;
+            p1 = dmul(qi, ri);
+        }
+        p1 = group_sum<SM_NT / 32, 0>(p1, sm.red);
+        if (tid == 0) Pqr[blockIdx.x] = p1;
+        grid.sync();
+        it = cur;
+        if (small) { stop = CONVERGED; break; }
+        if (it >= max_it) { stop = NOTCONV; break; }
+        const double qr = all_reduce_partials(Pqr, nt, sm.red);
+        const double denom = dmul(y, w);
+        y = qr;
+        if (tiny(denom)) { stop = BREAKDOWN; which = 1; bd_it = it + 1; break; }
+        beta = ddiv(dmul(qr, a), denom);
+    }
+    if (row >= 0) V.x[row] = xi;  // final iterate, or the snapshot before a breakdown
+    if (blockIdx.x == 0 && tid == 0) {
+        st->it = it;
+        st->stop = stop;
+        st->which = which;
+        st->bd_it = bd_it;
+    }
+}
+
+}  // namespace mcr

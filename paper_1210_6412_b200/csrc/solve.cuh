@@ -1,0 +1,327 @@
+// solve.cuh -- solve drivers: kernel launchers (PDL), the row-shard exchange points, and the
+// Jacobi / BiCGStab loops that enqueue batches of device-resident iterations.
+#pragma once
+
+namespace {
+
+void set_state(mcr_matrix* h, double tol, int64_t max_it) {
+    SolveState& s = *h->h_st;
+    std::memset(&s, 0, sizeof(s));
+    s.tol = tol;
+    s.max_it = max_it;
+    s.y = s.a = s.w = 1.0;
+    s.seqdots = h->seqdots;
+    s.sharded = h->sharded() ? 1 : 0;
+}
+
+int read_state(mcr_matrix* h) {
+    CK(cudaMemcpyAsync(h->h_st, h->st, sizeof(SolveState), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return MCR_OK;
+}
+
+// ---------------------------------------------------------------- kernel launchers
+// Every solve kernel goes out with programmatic stream serialization (PDL): the next kernel
+// of the chain is scheduled while the current one drains, and waits in griddepcontrol.wait.
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem,
+                cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
+template <int EPI>
+void launch_mv(mcr_matrix* h, bool offdiag, const double* x, const Vecs& V, int64_t* launches) {
+    if (h->storage == MCR_STORAGE_DENSE) {
+        launch_pdl(k_dense<EPI>, h->nslabs, 32, DENSE_SMEM, h->stream, (const double*)h->dense,
+                   (int)h->n, (int)((h->n + 1) & ~1ll), x, V, h->st);
+    } else if (h->use_sell) {
+        const auto& S = offdiag ? h->rsell : h->sell;
+        launch_pdl(k_sell<EPI>, S.nwin * (SELL_W / SELL_CTA), SELL_CTA, 0, h->stream,
+                   Sell{S.sptr, S.perm, S.col, S.val, S.nwin}, x, V, h->st);
+    } else {
+        launch_pdl(k_spmv<EPI>, h->spmv_grid, SP_THREADS, SP_SMEM, h->stream,
+                   offdiag ? csr_off(h) : csr_full(h), x, V, h->st);
+    }
+    ++*launches;
+}
+
+template <int PH>
+void launch_phase(mcr_matrix* h, const Vecs& V, int64_t* launches) {
+    launch_pdl(k_phase<PH>, h->nchunks(), CHUNK_NT, 0, h->stream, V, (int)h->n, h->st);
+    ++*launches;
+}
+
+template <int W>
+void launch_seqdot(mcr_matrix* h, const Vecs& V, int64_t* launches) {
+    if (!h->seqdots) return;
+    launch_pdl(k_seqdot<W>, 1, SEQ_NT, 0, h->stream, V, (int)h->n, h->st);
+    ++*launches;
+}
+
+// ---------------------------------------------------------------- sharded exchange points
+// One reduction point of a row-sharded solve: every rank's SEND_SLOTS partials (written by
+// the producing kernel's last CTA into st->send) are exchanged, then k_finalize<W> reduces them
+// in rank order and takes the scalar step. `buf` != null also allgathers that full vector in
+// the same step (Jacobi: the iterate just written).
+template <int W>
+int exchange_point(mcr_matrix* h, double* buf, int64_t* launches) {
+    Transport& T = *h->comm;
+    const double* send = h->st->send;
+    const int rc = buf ? T.allgather_and_slots(buf, (size_t)h->chunk, send, h->recv, SEND_SLOTS,
+                                               h->stream)
+                       : T.gather_slots(send, h->recv, SEND_SLOTS, h->stream);
+    if (rc) return fail(MCR_CUDA_ERROR, std::string(T.kind()) + " exchange: " + T.err);
+    launch_pdl(k_finalize<W>, 1, 32, 0, h->stream, h->st, (const double*)h->recv, h->world);
+    ++*launches;
+    CK(cudaGetLastError());
+    return MCR_OK;
+}
+
+int allgather_full(mcr_matrix* h, double* buf) {
+    Transport& T = *h->comm;
+    if (T.allgather(buf, (size_t)h->chunk, h->stream))
+        return fail(MCR_CUDA_ERROR, std::string(T.kind()) + " allgather: " + T.err);
+    return MCR_OK;
+}
+
+// Peer-to-peer mode: the producers already stored their rows into every peer's copy; a slot
+// exchange orders those stores before any rank's next gather (every rank's producer kernel
+// has retired -- with a system-scope fence -- before it enters the exchange).
+int p2p_barrier(mcr_matrix* h) {
+    Transport& T = *h->comm;
+    if (T.gather_slots(h->st->send, h->recv, SEND_SLOTS, h->stream))
+        return fail(MCR_CUDA_ERROR, std::string(T.kind()) + " barrier: " + T.err);
+    return MCR_OK;
+}
+
+// max|b - M x| into st->resid; x is the full (gathered) vector.
+int residual_into_state(mcr_matrix* h, const double* x, int64_t* launches) {
+    Vecs V = base_vecs(h);
+    launch_mv<EPI_RESID>(h, false, x, V, launches);
+    CK(cudaGetLastError());
+    if (h->sharded()) TRY(exchange_point<FIN_RESID>(h, nullptr, launches));
+    return MCR_OK;
+}
+
+// b -> V_B; x0 (this handle's rows) -> own slice of the full vector `x0_slot`, gathered when
+// sharded; no x0 means zeros.
+int prepare_inputs(mcr_matrix* h, const double* d_b, const double* d_x0, int x0_slot) {
+    const size_t bytes = sizeof(double) * (size_t)h->n;
+    CK(cudaMemcpyAsync(h->vec(V_B), d_b, bytes, cudaMemcpyDeviceToDevice, h->stream));
+    double* full = h->vec(x0_slot);
+    if (d_x0) {
+        CK(cudaMemcpyAsync(full + h->roff, d_x0, bytes, cudaMemcpyDeviceToDevice, h->stream));
+        if (h->sharded()) TRY(allgather_full(h, full));
+    } else {
+        CK(cudaMemsetAsync(full, 0, sizeof(double) * (size_t)h->n_full(), h->stream));
+    }
+    return MCR_OK;
+}
+
+// ZeroDiagonal must be decided identically on every rank before any sweep (a rank that
+// returned early would leave its peers waiting in a collective): exchange each rank's first
+// zero-diagonal row and take the smallest.
+int global_first_zero(mcr_matrix* h, long long* out) {
+    if (!h->sharded()) {
+        *out = h->first_zero;
+        return MCR_OK;
+    }
+    double mine[SEND_SLOTS] = {(double)h->first_zero, 0.0, 0.0, 0.0};
+    CK(cudaMemcpyAsync(h->st->send, mine, sizeof(mine), cudaMemcpyHostToDevice, h->stream));
+    Transport& T = *h->comm;
+    if (T.gather_slots(h->st->send, h->recv, SEND_SLOTS, h->stream))
+        return fail(MCR_CUDA_ERROR, std::string(T.kind()) + " exchange: " + T.err);
+    std::vector<double> all((size_t)h->world * SEND_SLOTS);
+    CK(cudaMemcpyAsync(all.data(), h->recv, sizeof(double) * all.size(), cudaMemcpyDeviceToHost,
+                       h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    long long best = -1;
+    for (int r = 0; r < h->world; ++r) {
+        const long long z = (long long)all[(size_t)r * SEND_SLOTS];
+        if (z >= 0 && (best < 0 || z < best)) best = z;
+    }
+    *out = best;
+    return MCR_OK;
+}
+
+// Batches grow 4, 8, ..., 32: a batch that overshoots the stop point only launches kernels
+// that return at their first instruction (and, sharded, exchanges that rewrite unchanged data).
+int next_batch(int cur) { return std::min(cur * 2, 32); }
+
+int jacobi_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double tol, int64_t max_it,
+                double* d_x_out, mcr_report* rep) {
+    TRY(ensure_work(h));
+    long long zero = -1;
+    TRY(global_first_zero(h, &zero));
+    if (zero >= 0) {
+        rep->zero_diagonal_index = zero;
+        return fail(MCR_ZERO_DIAGONAL, "zero diagonal entry in row " + std::to_string(zero));
+    }
+    TRY(ensure_offdiag(h));
+    TRY(prepare_inputs(h, d_b, d_x0, V_X));
+    set_state(h, tol, max_it);
+    CK(cudaMemcpyAsync(h->st, h->h_st, sizeof(SolveState), cudaMemcpyHostToDevice, h->stream));
+    Vecs V = base_vecs(h);
+    CK(cudaEventRecord(h->ev0, h->stream));
+    int64_t launched = 0, sweeps = 0;
+    int batch = 4;
+    if (h->small_grid > 0) {
+        CK(cudaMemsetAsync(h->maxslot, 0, 3 * sizeof(unsigned long long), h->stream));
+        Csr R = csr_off(h);
+        void* args[] = {&R, &V, &h->st, &h->maxslot};
+        CK(cudaLaunchCooperativeKernel((void*)k_jacobi_small, h->small_grid, SM_NT, args, 0, h->stream));
+        ++launched;
+        TRY(read_state(h));
+    } else for (;;) {
+        const int k = (int)std::min<int64_t>(batch, max_it - sweeps);
+        for (int i = 0; i < k; ++i) {
+            launch_mv<EPI_JACOBI>(h, true, nullptr, V, &launched);
+            if (h->sharded()) {  // sweep s writes buffer s & 1: gather it with the partial max
+                const int64_t sweep = sweeps + i + 1;
+                double* wrote = (sweep & 1) ? h->vec(V_X1) : h->vec(V_X);
+                TRY(exchange_point<FIN_JACOBI>(h, h->p2p ? nullptr : wrote, &launched));
+            }
+        }
+        CK(cudaGetLastError());
+        sweeps += k;
+        TRY(read_state(h));
+        if (h->h_st->stop || sweeps >= max_it) break;
+        batch = next_batch(batch);
+    }
+    const long long it = h->h_st->it;
+    const double* x = (it & 1) ? h->vec(V_X1) : h->vec(V_X);  // full iterate (gathered)
+    TRY(residual_into_state(h, x, &launched));
+    CK(cudaEventRecord(h->ev1, h->stream));
+    TRY(read_state(h));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+    if (d_x_out)
+        CK(cudaMemcpyAsync(d_x_out, x + h->roff, sizeof(double) * (size_t)h->n,
+                           cudaMemcpyDeviceToDevice, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    const SolveState& s = *h->h_st;
+    rep->iterations = s.it;
+    rep->converged = s.stop == CONVERGED;
+    rep->residual_inf = s.resid;
+    rep->device_seconds = ms * 1e-3;
+    rep->kernel_launches = launched;
+    return s.stop == CONVERGED ? MCR_OK : MCR_NOT_CONVERGED;
+}
+
+int bicgstab_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double tol,
+                  int64_t max_it, double* d_x_out, mcr_report* rep) {
+    TRY(ensure_work(h));
+    TRY(prepare_inputs(h, d_b, d_x0, V_X));
+    set_state(h, tol, max_it);
+    CK(cudaMemcpyAsync(h->st, h->h_st, sizeof(SolveState), cudaMemcpyHostToDevice, h->stream));
+    Vecs V = base_vecs(h);
+    const bool sh = h->sharded();
+    CK(cudaEventRecord(h->ev0, h->stream));
+    int64_t launched = 0, iters = 0;
+    int batch = 4;
+    if (h->small_grid > 0 && !h->seqdots) {
+        CK(cudaMemsetAsync(h->maxslot, 0, 3 * sizeof(unsigned long long), h->stream));
+        Csr A = csr_full(h);
+        double* parts = h->P;
+        int pstride = h->nunits;  // four partial slots of nunits >= ntiles doubles each
+        void* args[] = {&A, &V, &h->st, &h->maxslot, &parts, &pstride};
+        CK(cudaLaunchCooperativeKernel((void*)k_bicg_small, h->small_grid, SM_NT, args, 0, h->stream));
+        ++launched;
+        TRY(read_state(h));
+        iters = max_it;  // the loop below has nothing left to do
+    } else {
+        // r = b - 1.0 * M x0, q = r, p = v = 0
+        launch_mv<EPI_S0>(h, false, h->vec(V_X), V, &launched);
+        launch_seqdot<SQ_S0>(h, V, &launched);
+        CK(cudaGetLastError());
+        if (sh) TRY(exchange_point<FIN_S0>(h, nullptr, &launched));
+        TRY(read_state(h));
+    }
+    double* p_full = h->vec(V_P);
+    double* s_full = h->vec(V_S);
+    while (!h->h_st->stop && iters < max_it) {
+        const int k = (int)std::min<int64_t>(batch, max_it - iters);
+        for (int i = 0; i < k; ++i) {
+            launch_phase<PH_A>(h, V, &launched);               // p = r + beta (p - w v)
+            if (sh) TRY(h->p2p ? p2p_barrier(h) : allgather_full(h, p_full));
+            launch_mv<EPI_V>(h, false, p_full, V, &launched);  // v = M p, q.v -> a
+            launch_seqdot<SQ_V>(h, V, &launched);
+            if (sh) TRY(exchange_point<FIN_V>(h, nullptr, &launched));
+            launch_phase<PH_C>(h, V, &launched);               // s = r - a v, max|s|
+            if (sh) TRY(h->p2p ? p2p_barrier(h) : allgather_full(h, s_full));
+            launch_mv<EPI_T>(h, false, s_full, V, &launched);  // t = M s, t.t, t.s -> w
+            launch_seqdot<SQ_T>(h, V, &launched);
+            if (sh) TRY(exchange_point<FIN_T>(h, nullptr, &launched));
+            launch_phase<PH_E>(h, V, &launched);               // x, r updates, q.r -> beta
+            launch_seqdot<SQ_E>(h, V, &launched);
+            if (sh) TRY(exchange_point<FIN_E>(h, nullptr, &launched));
+        }
+        CK(cudaGetLastError());
+        iters += k;
+        TRY(read_state(h));
+        batch = next_batch(batch);
+    }
+    if (sh) TRY(allgather_full(h, h->vec(V_X)));  // this rank's x is its slice of V_X
+    TRY(residual_into_state(h, h->vec(V_X), &launched));
+    CK(cudaEventRecord(h->ev1, h->stream));
+    TRY(read_state(h));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+    if (d_x_out)
+        CK(cudaMemcpyAsync(d_x_out, V.x, sizeof(double) * (size_t)h->n, cudaMemcpyDeviceToDevice,
+                           h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    const SolveState& s = *h->h_st;
+    rep->residual_inf = s.resid;
+    rep->device_seconds = ms * 1e-3;
+    rep->kernel_launches = launched;
+    rep->converged = s.stop == CONVERGED;
+    if (s.stop == BREAKDOWN) {
+        rep->iterations = s.bd_it;
+        rep->breakdown_which = s.which;
+        rep->breakdown_iteration = s.bd_it;
+        const char* names[] = {"", "y_prev*w", "q*v", "t*t"};
+        return fail(MCR_BREAKDOWN, std::string("breakdown: ") + names[s.which & 3] +
+                                       " vanished at iteration " + std::to_string(s.bd_it));
+    }
+    rep->iterations = s.it;
+    return s.stop == CONVERGED ? MCR_OK : MCR_NOT_CONVERGED;
+}
+
+void report_init(mcr_report* rep) {
+    std::memset(rep, 0, sizeof(*rep));
+    rep->zero_diagonal_index = -1;
+}
+
+// Host-pointer front end: stage b / x0 in the handle's workspace, run, copy x back.
+template <class Impl>
+int host_solve(mcr_matrix* h, const double* b, const double* x0, double tol, int64_t max_it,
+               double* x_out, mcr_report* rep, Impl impl) {
+    const size_t bytes = sizeof(double) * (size_t)h->n;
+    TRY(ensure_work(h));
+    double* db = h->vec(V_R);   // scratch slots: overwritten by the solve only after the copy
+    double* dx = h->vec(V_Q);
+    CK(cudaMemcpyAsync(db, b, bytes, cudaMemcpyHostToDevice, h->stream));
+    if (x0) CK(cudaMemcpyAsync(dx, x0, bytes, cudaMemcpyHostToDevice, h->stream));
+    double* dout = h->vec(V_V);
+    int rc = impl(h, db, x0 ? dx : nullptr, tol, max_it, dout, rep);
+    if (rc == MCR_OK || rc == MCR_NOT_CONVERGED || rc == MCR_BREAKDOWN) {
+        const double* src = dout;
+        if (rc == MCR_BREAKDOWN) src = h->vec(V_X) + h->roff;  // snapshot: x before that iteration
+        CK(cudaMemcpyAsync(x_out, src, bytes, cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+    }
+    return rc;
+}
+
+}  // namespace

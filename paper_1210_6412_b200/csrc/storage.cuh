@@ -1,0 +1,375 @@
+// storage.cuh -- building a handle's device storage: upload and validation, diagonal, row tiles,
+// Jacobi's off-diagonal copy, SELL and dense layouts, the C5 generator and device-side CSRs.
+#pragma once
+
+namespace {
+
+// Off-diagonal copy R: row lengths from k_diag, exclusive scan (CUB), order-preserving split.
+int build_sell(mcr_matrix* h, bool offdiag, mcr_matrix::SellDev* S) {
+    const int n = (int)h->n;
+    S->nwin = (n + SELL_W - 1) / SELL_W;
+    const int nslices = S->nwin * SELL_SLICES;
+    TRY(dalloc(h, &S->perm, (size_t)S->nwin * SELL_W));
+    TRY(dalloc(h, &S->swidth, (size_t)nslices + 1));
+    TRY(dalloc(h, &S->sptr, (size_t)nslices + 1));
+    CK(cudaMemsetAsync(S->swidth + nslices, 0, sizeof(long long), h->stream));
+    k_sell_rank<<<S->nwin, SELL_W, 0, h->stream>>>(h->rp, h->offlen, n, offdiag ? 1 : 0, S->perm,
+                                                   S->swidth);
+    CK(cudaGetLastError());
+    size_t tmp = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, S->swidth, S->sptr, nslices + 1, h->stream));
+    void* dtmp = nullptr;
+    CK(cudaMallocAsync(&dtmp, tmp, h->stream));
+    CK(cub::DeviceScan::ExclusiveSum(dtmp, tmp, S->swidth, S->sptr, nslices + 1, h->stream));
+    CK(cudaFreeAsync(dtmp, h->stream));
+    CK(cudaMemcpyAsync(&S->slots, S->sptr + nslices, sizeof(long long), cudaMemcpyDeviceToHost,
+                       h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    TRY(dalloc(h, &S->col, (size_t)S->slots));
+    TRY(dalloc(h, &S->val, (size_t)S->slots));
+    const int rows = S->nwin * SELL_W;
+    k_sell_fill<<<(rows + 255) / 256, 256, 0, h->stream>>>(h->rp, h->col, h->val, S->sptr, S->perm,
+                                                           rows, offdiag ? 1 : 0, S->col, S->val);
+    CK(cudaGetLastError());
+    return MCR_OK;
+}
+
+int ensure_offdiag(mcr_matrix* h) {
+    if (h->r_ready || h->storage != MCR_STORAGE_CSR) return MCR_OK;
+    if (h->use_sell) {
+        TRY(build_sell(h, true, &h->rsell));
+        h->r_ready = true;
+        return MCR_OK;
+    }
+    const int n = (int)h->n;
+    TRY(dalloc(h, &h->rrp, (size_t)n + 1 + CSR_PAD));
+    size_t tmp = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, h->offlen, h->rrp, n + 1, h->stream));
+    void* dtmp = nullptr;
+    CK(cudaMallocAsync(&dtmp, tmp, h->stream));
+    CK(cub::DeviceScan::ExclusiveSum(dtmp, tmp, h->offlen, h->rrp, n + 1, h->stream));
+    CK(cudaFreeAsync(dtmp, h->stream));
+    long long roff = 0;
+    CK(cudaMemcpyAsync(&roff, h->rrp + n, sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    TRY(dalloc(h, &h->rcol, (size_t)roff + CSR_PAD));
+    TRY(dalloc(h, &h->rval, (size_t)roff + CSR_PAD));
+    const int threads = 256;
+    const int blocks = (int)std::min<long long>(((long long)n * 32 + threads - 1) / threads, 1 << 20);
+    if (n > 0)
+        k_split_offdiag<<<blocks, threads, 0, h->stream>>>(h->rp, h->col, h->val, n, h->roff,
+                                                           h->rrp, h->rcol, h->rval);
+    CK(cudaGetLastError());
+    TRY(dalloc(h, &h->rdesc, (size_t)h->ntiles));
+    if (h->ntiles > 0)
+        k_tile_desc<<<(h->ntiles + 255) / 256, 256, 0, h->stream>>>(h->rrp, h->tile_row, h->ntiles,
+                                                                     h->rdesc);
+    CK(cudaGetLastError());
+    h->r_ready = true;
+    return MCR_OK;
+}
+
+// Greedy tiles: consecutive rows while rows <= TILE_ROWS and entries <= TILE_NNZ; a row with
+// more than TILE_NNZ entries is a tile of its own.
+std::vector<int> make_tiles(int64_t n, const int64_t* rs, long long* max_row) {
+    std::vector<int> t;
+    t.reserve((size_t)(n / 64 + 2));
+    t.push_back(0);
+    long long mr = 0;
+    int64_t r = 0;
+    while (r < n) {
+        const int64_t start = r;
+        int64_t nnz = 0;
+        while (r < n && r - start < TILE_ROWS) {
+            const int64_t len = rs[r + 1] - rs[r];
+            mr = std::max<long long>(mr, len);
+            if (nnz + len > TILE_NNZ && r > start) break;
+            nnz += len;
+            ++r;
+            if (nnz > TILE_NNZ) break;
+        }
+        t.push_back((int)r);
+    }
+    *max_row = mr;
+    return t;
+}
+
+
+}  // namespace
+
+static int set_kernel_attributes() {
+    const int sp = (int)SP_SMEM;
+    CK(cudaFuncSetAttribute(k_spmv<EPI_Y>, cudaFuncAttributeMaxDynamicSharedMemorySize, sp));
+    CK(cudaFuncSetAttribute(k_spmv<EPI_RESID>, cudaFuncAttributeMaxDynamicSharedMemorySize, sp));
+    CK(cudaFuncSetAttribute(k_spmv<EPI_JACOBI>, cudaFuncAttributeMaxDynamicSharedMemorySize, sp));
+    CK(cudaFuncSetAttribute(k_spmv<EPI_S0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sp));
+    CK(cudaFuncSetAttribute(k_spmv<EPI_V>, cudaFuncAttributeMaxDynamicSharedMemorySize, sp));
+    CK(cudaFuncSetAttribute(k_spmv<EPI_T>, cudaFuncAttributeMaxDynamicSharedMemorySize, sp));
+    return MCR_OK;
+}
+
+// Rows [h->roff, h->roff + n) of an h->n_global system (the whole system on one GPU);
+// column indices are global.
+int finish_create(mcr_matrix* h, int64_t n, const int64_t* rs, int storage,
+                         std::vector<int>* pre_tiles = nullptr);
+
+int init_handle(mcr_matrix* h) {
+    TRY(keep_pool_memory(h->device));
+    CK(cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking));
+    h->stream = h->own_stream;
+    CK(cudaEventCreate(&h->ev0));
+    CK(cudaEventCreate(&h->ev1));
+    TRY(dalloc(h, &h->st, 1));
+    CK(cudaMemsetAsync(h->st, 0, sizeof(SolveState), h->stream));
+    return MCR_OK;
+}
+
+int alloc_csr(mcr_matrix* h, int64_t n, int64_t nnz) {
+    h->nnz = nnz;
+    if (!h->rp) TRY(dalloc(h, &h->rp, (size_t)n + 1 + CSR_PAD));
+    TRY(dalloc(h, &h->col, (size_t)nnz + CSR_PAD));
+    TRY(dalloc(h, &h->val, (size_t)nnz + CSR_PAD));
+    TRY(dalloc(h, &h->d, (size_t)n));
+    TRY(dalloc(h, &h->offlen, (size_t)n + 1));
+    return MCR_OK;
+}
+
+int create_impl(mcr_matrix* h, int64_t n, const int64_t* rs, const int64_t* col,
+                       const double* val, int storage) {
+    TRY(init_handle(h));
+    if (n == 0) return MCR_OK;
+    const int64_t nnz = rs[n];
+    TRY(alloc_csr(h, n, nnz));
+    CK(cudaMemcpyAsync(h->rp, rs, sizeof(long long) * (size_t)(n + 1), cudaMemcpyHostToDevice,
+                       h->stream));
+    CK(cudaMemcpyAsync(h->val, val, sizeof(double) * (size_t)nnz, cudaMemcpyHostToDevice,
+                       h->stream));
+    // int64 columns -> int32 on the device, range-checked
+    {
+        long long* tmp = nullptr;
+        int* bad = nullptr;
+        CK(cudaMallocAsync((void**)&tmp, sizeof(long long) * (size_t)std::max<int64_t>(nnz, 1),
+                           h->stream));
+        CK(cudaMallocAsync((void**)&bad, 2 * sizeof(int), h->stream));
+        CK(cudaMemsetAsync(bad, 0, 2 * sizeof(int), h->stream));
+        CK(cudaMemcpyAsync(tmp, col, sizeof(long long) * (size_t)nnz, cudaMemcpyHostToDevice,
+                           h->stream));
+        if (nnz > 0) {
+            k_col64to32<<<(int)std::min<int64_t>((nnz + 255) / 256, 1 << 16), 256, 0, h->stream>>>(
+                tmp, h->col, nnz, (int)h->n_global, bad);
+            k_check_rows<<<(int)std::min<int64_t>((n + 255) / 256, 1 << 16), 256, 0, h->stream>>>(
+                h->rp, h->col, (int)n, bad + 1);
+        }
+        CK(cudaGetLastError());
+        int hbad[2] = {0, 0};
+        CK(cudaMemcpyAsync(hbad, bad, 2 * sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaFreeAsync(tmp, h->stream));
+        CK(cudaFreeAsync(bad, h->stream));
+        // the row tiles are cut on the host while the copies are in flight
+        std::vector<int> tiles = make_tiles(n, rs, &h->max_row);
+        CK(cudaStreamSynchronize(h->stream));
+        if (hbad[0]) return fail(MCR_DIMENSION, "column index out of range");
+        if (hbad[1]) return fail(MCR_DIMENSION, "rows must be sorted by column without duplicates");
+        return finish_create(h, n, rs, storage, &tiles);
+    }
+}
+
+// A handle from a CSR already on the device (int64 row starts, int32 columns), copied.
+int create_from_device(int64_t n, int64_t nnz, const long long* d_rp, const int* d_col,
+                              const double* d_val, int device, int storage, mcr_matrix** out) {
+    DeviceGuard g(device);
+    mcr_matrix* h = new mcr_matrix();
+    h->device = device;
+    h->n = n;
+    h->n_global = n;
+    h->chunk = n;
+    int rc = [&]() -> int {
+        TRY(init_handle(h));
+        if (n == 0) return MCR_OK;
+        TRY(alloc_csr(h, n, nnz));
+        CK(cudaMemcpyAsync(h->rp, d_rp, sizeof(long long) * (size_t)(n + 1), cudaMemcpyDeviceToDevice, h->stream));
+        CK(cudaMemcpyAsync(h->col, d_col, sizeof(int) * (size_t)nnz, cudaMemcpyDeviceToDevice, h->stream));
+        CK(cudaMemcpyAsync(h->val, d_val, sizeof(double) * (size_t)nnz, cudaMemcpyDeviceToDevice, h->stream));
+        std::vector<int64_t> rs((size_t)n + 1);
+        CK(cudaMemcpyAsync(rs.data(), d_rp, sizeof(int64_t) * rs.size(), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        return finish_create(h, n, rs.data(), storage);
+    }();
+    if (rc != MCR_OK) {
+        std::string msg = g_err;
+        mcr_matrix_destroy(h);
+        g_err = msg;
+        return rc;
+    }
+    *out = h;
+    return MCR_OK;
+}
+
+// Poisson(mean) inverse-CDF thresholds on 2^64 (generator.cuh); restated in oracle.c.
+void poisson_thresholds(double mean, uint64_t* thr) {
+    double p = std::exp(-mean), cdf = 0.0;
+    for (int k = 0; k < GEN_KMAX; ++k) {
+        cdf += p;
+        const double t = cdf * 18446744073709551616.0;
+        thr[k] = t >= 18446744073709551616.0 ? UINT64_MAX : (uint64_t)t;
+        p = (p * mean) / (double)(k + 1);
+    }
+}
+
+// Rows [h->roff, h->roff + h->n) of the row-keyed synthetic system, built on the device.
+int generate_impl(mcr_matrix* h, const GenParams& P, int storage) {
+    TRY(init_handle(h));
+    const int64_t n = h->n;
+    if (n == 0) return MCR_OK;
+    TRY(dalloc(h, &h->rp, (size_t)n + 1 + CSR_PAD));
+    long long* len = nullptr;
+    CK(cudaMallocAsync((void**)&len, sizeof(long long) * (size_t)(n + 1), h->stream));
+    CK(cudaMemsetAsync(len + n, 0, sizeof(long long), h->stream));
+    const int grid = (int)std::min<int64_t>((n + 255) / 256, 1 << 16);
+    k_gen_count<<<grid, 256, 0, h->stream>>>(P, (long long)n, len);
+    CK(cudaGetLastError());
+    size_t tmp = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, len, h->rp, n + 1, h->stream));
+    void* dtmp = nullptr;
+    CK(cudaMallocAsync(&dtmp, tmp, h->stream));
+    CK(cub::DeviceScan::ExclusiveSum(dtmp, tmp, len, h->rp, n + 1, h->stream));
+    CK(cudaFreeAsync(dtmp, h->stream));
+    CK(cudaFreeAsync(len, h->stream));
+    std::vector<int64_t> rs((size_t)n + 1);
+    CK(cudaMemcpyAsync(rs.data(), h->rp, sizeof(int64_t) * rs.size(), cudaMemcpyDeviceToHost,
+                       h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    TRY(alloc_csr(h, n, rs[(size_t)n]));
+    k_gen_fill<<<(int)std::min<int64_t>((n + 127) / 128, 1 << 20), 128, 0, h->stream>>>(
+        P, (long long)n, h->rp, h->col, h->val);
+    CK(cudaGetLastError());
+    return finish_create(h, n, rs.data(), storage);
+}
+
+// Device CSR (rp/col/val) in place; `rs` = host copy of the row starts. Diagonal, tiles or
+// dense slabs, kernel attributes.
+int finish_create(mcr_matrix* h, int64_t n, const int64_t* rs, int storage,
+                         std::vector<int>* pre_tiles) {
+    const int64_t nnz = h->nnz;
+    const bool dense = !h->sharded() &&
+                       (storage == MCR_STORAGE_DENSE ||
+                        (storage == MCR_STORAGE_AUTO && n >= 1024 &&
+                         (double)nnz * 3.0 >= 2.0 * (double)n * (double)n));
+    h->storage = dense ? MCR_STORAGE_DENSE : MCR_STORAGE_CSR;
+    // diagonal, first zero-diagonal row, off-diagonal row lengths
+    {
+        unsigned long long* fz = nullptr;
+        CK(cudaMallocAsync((void**)&fz, sizeof(unsigned long long), h->stream));
+        CK(cudaMemsetAsync(fz, 0xff, sizeof(unsigned long long), h->stream));
+        CK(cudaMemsetAsync(h->offlen + n, 0, sizeof(long long), h->stream));
+        k_diag<<<(int)std::min<int64_t>((n + 255) / 256, 1 << 16), 256, 0, h->stream>>>(
+            h->rp, h->col, h->val, (int)n, (long long)h->roff, h->d, h->offlen, fz);
+        CK(cudaGetLastError());
+        unsigned long long hfz = 0;
+        CK(cudaMemcpyAsync(&hfz, fz, sizeof(hfz), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaFreeAsync(fz, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        h->first_zero = hfz == ~0ull ? -1 : (long long)hfz + h->roff;  // global row
+    }
+    std::vector<int> tiles;
+    if (pre_tiles) tiles.swap(*pre_tiles);
+    else tiles = make_tiles(n, rs, &h->max_row);
+    if (dense) {
+        h->nslabs = (int)((n + DSLAB - 1) / DSLAB);
+        const int64_t npad = (n + 1) & ~1ll;  // column pairs
+        const size_t cnt = (size_t)h->nslabs * DSLAB * (size_t)npad;
+        TRY(dalloc(h, &h->dense, cnt));
+        CK(cudaMemsetAsync(h->dense, 0, sizeof(double) * cnt, h->stream));
+        k_dense_build<<<(int)n, 256, 0, h->stream>>>(h->rp, h->col, h->val, (int)n, (int)npad,
+                                                     h->dense);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(h->stream));
+        dfree(h, h->col, (size_t)nnz + CSR_PAD);
+        dfree(h, h->val, (size_t)nnz + CSR_PAD);
+        dfree(h, h->offlen, (size_t)n + 1);
+        CK(cudaFuncSetAttribute(k_dense<EPI_Y>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DENSE_SMEM));
+        CK(cudaFuncSetAttribute(k_dense<EPI_RESID>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DENSE_SMEM));
+        CK(cudaFuncSetAttribute(k_dense<EPI_JACOBI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DENSE_SMEM));
+        CK(cudaFuncSetAttribute(k_dense<EPI_S0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DENSE_SMEM));
+        CK(cudaFuncSetAttribute(k_dense<EPI_V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DENSE_SMEM));
+        CK(cudaFuncSetAttribute(k_dense<EPI_T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DENSE_SMEM));
+    } else {
+        h->ntiles = (int)tiles.size() - 1;
+        // SELL streams rows without shared-memory staging, but its epilogue operands are
+        // gathered through the row permutation; measured on C2 (profiles/) the TMA-staged
+        // tiles win (54 vs 70 us per Jacobi sweep), so SELL is opt-in.
+        h->use_sell = storage == MCR_STORAGE_SELL && !h->sharded();
+        if (h->use_sell) TRY(build_sell(h, false, &h->sell));
+        TRY(set_kernel_attributes());
+        int sms = 0, per_sm = 0;
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv<EPI_V>, SP_THREADS, SP_SMEM));
+        h->spmv_grid = std::max(1, std::min(h->ntiles, sms * std::max(per_sm, 1)));
+        int pj = 0, pb = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pj, k_jacobi_small, SM_NT, 0));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pb, k_bicg_small, SM_NT, 0));
+        const int coresident = sms * std::min(pj, pb);
+        // one tile per CTA keeps the per-sweep critical path to a single tile
+        if (!h->use_sell && !h->sharded() && storage != MCR_STORAGE_TILES_STREAM &&
+            h->ntiles <= coresident && h->ntiles <= 2 * sms)
+            h->small_grid = h->ntiles;
+        TRY(dalloc(h, &h->maxslot, 3));
+        TRY(dalloc(h, &h->tile_row, tiles.size()));
+        CK(cudaMemcpyAsync(h->tile_row, tiles.data(), sizeof(int) * tiles.size(),
+                           cudaMemcpyHostToDevice, h->stream));
+        std::vector<TileDesc> desc((size_t)h->ntiles);
+        for (int t = 0; t < h->ntiles; ++t)
+            desc[(size_t)t] = TileDesc{rs[tiles[(size_t)t]], rs[tiles[(size_t)t + 1]], tiles[(size_t)t],
+                                       tiles[(size_t)t + 1]};
+        TRY(dalloc(h, &h->desc, desc.size()));
+        CK(cudaMemcpyAsync(h->desc, desc.data(), sizeof(TileDesc) * desc.size(),
+                           cudaMemcpyHostToDevice, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+    }
+    return MCR_OK;
+}
+
+int check_csr(int64_t n, const int64_t* rstart, const int64_t* col, const double* nonzero) {
+    if (n < 0 || n >= INT_MAX) return fail(MCR_DIMENSION, "dimension out of range");
+    if (n > 0 && (!rstart || (rstart[n] > 0 && (!col || !nonzero))))
+        return fail(MCR_INVALID_ARGUMENT, "NULL CSR array");
+    if (n > 0) {
+        if (rstart[0] != 0) return fail(MCR_DIMENSION, "malformed rstart vector");
+        for (int64_t i = 0; i < n; ++i)
+            if (rstart[i + 1] < rstart[i]) return fail(MCR_DIMENSION, "rstart must be nondecreasing");
+    }
+    return MCR_OK;
+}
+
+int create_handle(int64_t n, const int64_t* rstart, const int64_t* col,
+                         const double* nonzero, int device, int storage,
+                         const std::shared_ptr<Transport>& comm, int64_t n_global, int64_t roff,
+                         int64_t chunk, mcr_matrix** out) {
+    int ndev = 0;
+    mcr_device_count(&ndev);
+    if (device < 0 || device >= ndev)
+        return fail(MCR_CUDA_ERROR, "no CUDA device " + std::to_string(device) + " (" +
+                                        std::to_string(ndev) + " visible)");
+    DeviceGuard g(device);
+    mcr_matrix* h = new mcr_matrix();
+    h->device = device;
+    h->n = n;
+    h->n_global = n_global;
+    h->roff = roff;
+    h->chunk = chunk;
+    if (comm) {
+        h->comm = comm;
+        h->world = comm->world;
+        h->rank = comm->rank;
+    }
+    int rc = create_impl(h, n, rstart, col, nonzero, storage);
+    if (rc != MCR_OK) {
+        std::string msg = g_err;
+        mcr_matrix_destroy(h);
+        g_err = msg;
+        return rc;
+    }
+    *out = h;
+    return MCR_OK;
+}
+
