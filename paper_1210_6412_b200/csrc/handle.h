@@ -5,12 +5,14 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <climits>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <cub/device/device_scan.cuh>
@@ -137,6 +139,8 @@ struct mcr_matrix {
     // diagonal + facts
     double* d = nullptr;
     long long first_zero = -1;
+    unsigned long long fz_host = ~0ull;  // D2H target of the first-zero-diagonal search
+    int bad_host[2] = {0, 0};            // D2H target of the upload checks
     long long max_row = 0;
     // workspace
     double* work = nullptr;

@@ -135,7 +135,7 @@ int alloc_csr(mcr_matrix* h, int64_t n, int64_t nnz) {
 }
 
 int create_impl(mcr_matrix* h, int64_t n, const int64_t* rs, const int64_t* col,
-                       const double* val, int storage) {
+                const double* val, int storage) {
     TRY(init_handle(h));
     if (n == 0) return MCR_OK;
     const int64_t nnz = rs[n];
@@ -144,34 +144,33 @@ int create_impl(mcr_matrix* h, int64_t n, const int64_t* rs, const int64_t* col,
                        h->stream));
     CK(cudaMemcpyAsync(h->val, val, sizeof(double) * (size_t)nnz, cudaMemcpyHostToDevice,
                        h->stream));
-    // int64 columns -> int32 on the device, range-checked
-    {
-        long long* tmp = nullptr;
-        int* bad = nullptr;
-        CK(cudaMallocAsync((void**)&tmp, sizeof(long long) * (size_t)std::max<int64_t>(nnz, 1),
-                           h->stream));
-        CK(cudaMallocAsync((void**)&bad, 2 * sizeof(int), h->stream));
-        CK(cudaMemsetAsync(bad, 0, 2 * sizeof(int), h->stream));
-        CK(cudaMemcpyAsync(tmp, col, sizeof(long long) * (size_t)nnz, cudaMemcpyHostToDevice,
-                           h->stream));
-        if (nnz > 0) {
-            k_col64to32<<<(int)std::min<int64_t>((nnz + 255) / 256, 1 << 16), 256, 0, h->stream>>>(
-                tmp, h->col, nnz, (int)h->n_global, bad);
-            k_check_rows<<<(int)std::min<int64_t>((n + 255) / 256, 1 << 16), 256, 0, h->stream>>>(
-                h->rp, h->col, (int)n, bad + 1);
-        }
-        CK(cudaGetLastError());
-        int hbad[2] = {0, 0};
-        CK(cudaMemcpyAsync(hbad, bad, 2 * sizeof(int), cudaMemcpyDeviceToHost, h->stream));
-        CK(cudaFreeAsync(tmp, h->stream));
-        CK(cudaFreeAsync(bad, h->stream));
-        // the row tiles are cut on the host while the copies are in flight
-        std::vector<int> tiles = make_tiles(n, rs, &h->max_row);
-        CK(cudaStreamSynchronize(h->stream));
-        if (hbad[0]) return fail(MCR_DIMENSION, "column index out of range");
-        if (hbad[1]) return fail(MCR_DIMENSION, "rows must be sorted by column without duplicates");
-        return finish_create(h, n, rs, storage, &tiles);
+    // int64 columns -> int32 on the device, range-checked, then the row-order check. (A host
+    // conversion sending half the bytes was measured slower: the host threads compete with
+    // the value copy for host memory bandwidth.)
+    long long* tmp = nullptr;
+    int* bad = nullptr;
+    CK(cudaMallocAsync((void**)&tmp, sizeof(long long) * (size_t)std::max<int64_t>(nnz, 1),
+                       h->stream));
+    CK(cudaMallocAsync((void**)&bad, 2 * sizeof(int), h->stream));
+    CK(cudaMemsetAsync(bad, 0, 2 * sizeof(int), h->stream));
+    CK(cudaMemcpyAsync(tmp, col, sizeof(long long) * (size_t)nnz, cudaMemcpyHostToDevice,
+                       h->stream));
+    if (nnz > 0) {
+        k_col64to32<<<(int)std::min<int64_t>((nnz + 255) / 256, 1 << 16), 256, 0, h->stream>>>(
+            tmp, h->col, nnz, (int)h->n_global, bad);
+        k_check_rows<<<(int)std::min<int64_t>((n + 255) / 256, 1 << 16), 256, 0, h->stream>>>(
+            h->rp, h->col, (int)n, bad + 1);
     }
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(h->bad_host, bad, 2 * sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaFreeAsync(tmp, h->stream));
+    CK(cudaFreeAsync(bad, h->stream));
+    // the row tiles are cut on the host while the copies are in flight
+    std::vector<int> tiles = make_tiles(n, rs, &h->max_row);
+    CK(cudaStreamSynchronize(h->stream));
+    if (h->bad_host[0]) return fail(MCR_DIMENSION, "column index out of range");
+    if (h->bad_host[1]) return fail(MCR_DIMENSION, "rows must be sorted by column without duplicates");
+    return finish_create(h, n, rs, storage, &tiles);
 }
 
 // A handle from a CSR already on the device (int64 row starts, int32 columns), copied.
@@ -256,7 +255,8 @@ int finish_create(mcr_matrix* h, int64_t n, const int64_t* rs, int storage,
                         (storage == MCR_STORAGE_AUTO && n >= 1024 &&
                          (double)nnz * 3.0 >= 2.0 * (double)n * (double)n));
     h->storage = dense ? MCR_STORAGE_DENSE : MCR_STORAGE_CSR;
-    // diagonal, first zero-diagonal row, off-diagonal row lengths
+    // diagonal, first zero-diagonal row (read back at the final synchronisation below),
+    // off-diagonal row lengths
     {
         unsigned long long* fz = nullptr;
         CK(cudaMallocAsync((void**)&fz, sizeof(unsigned long long), h->stream));
@@ -265,11 +265,9 @@ int finish_create(mcr_matrix* h, int64_t n, const int64_t* rs, int storage,
         k_diag<<<(int)std::min<int64_t>((n + 255) / 256, 1 << 16), 256, 0, h->stream>>>(
             h->rp, h->col, h->val, (int)n, (long long)h->roff, h->d, h->offlen, fz);
         CK(cudaGetLastError());
-        unsigned long long hfz = 0;
-        CK(cudaMemcpyAsync(&hfz, fz, sizeof(hfz), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaMemcpyAsync(&h->fz_host, fz, sizeof(h->fz_host), cudaMemcpyDeviceToHost,
+                           h->stream));  // a handle field: outlives any early return
         CK(cudaFreeAsync(fz, h->stream));
-        CK(cudaStreamSynchronize(h->stream));
-        h->first_zero = hfz == ~0ull ? -1 : (long long)hfz + h->roff;  // global row
     }
     std::vector<int> tiles;
     if (pre_tiles) tiles.swap(*pre_tiles);
@@ -326,6 +324,7 @@ int finish_create(mcr_matrix* h, int64_t n, const int64_t* rs, int storage,
                            cudaMemcpyHostToDevice, h->stream));
         CK(cudaStreamSynchronize(h->stream));
     }
+    h->first_zero = h->fz_host == ~0ull ? -1 : (long long)h->fz_host + h->roff;  // global row
     return MCR_OK;
 }
 

@@ -9,6 +9,6 @@ for v in "$@"; do
   s=$(echo $v | sed -E 's/.*s([0-9]+)t.*/\1/'); t=$(echo $v | sed -E 's/.*t([0-9]+)$/\1/')
   mkdir -p build/variants/$v
   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC -Xcompiler -fvisibility=hidden -shared -Iinclude \
-    -DMCR_SP_BATCH=$b -DMCR_SP_MINB=$m -DMCR_SP_STAGES=$s -DMCR_TILE_NNZ=$t -o build/variants/$v/libmcr.so paper_1210_6412_b200/csrc/mcr.cu &
+    -DMCR_SP_BATCH=$b -DMCR_SP_MINB=$m -DMCR_SP_STAGES=$s -DMCR_TILE_NNZ=$t -o build/variants/$v/libmcr.so paper_1210_6412_b200/csrc/mcr.cu paper_1210_6412_b200/csrc/formats.cpp &
 done
 wait
