@@ -163,25 +163,49 @@ def reference_module():
         return None
 
 
-def cpu_solve_pair(m, b, threads: int):
-    """One full Jacobi + BiCGStab solve pair of the reference's CPU path. Returns
-    (seconds, kind, iterations). kind 'reference' = mcreach itself (baseline/_ref),
-    'port' = the C restatement in oracle/ (when the reference is not installed)."""
+def cpu_solve_pair(m, b, threads: int, jacobi_cap: int = 0):
+    """One Jacobi + BiCGStab solve pair of the reference's CPU path. Returns (seconds, kind,
+    iterations, note). kind 'reference' = mcreach itself (baseline/_ref), 'port' = the C
+    restatement in oracle/ (when the reference is not installed). Solver failures are timed
+    like successes (bench.py:184-187 records them in-row). jacobi_cap > 0 bounds the sample:
+    Jacobi runs `jacobi_cap` sweeps and its time is scaled to the 10 000-sweep budget (C3,
+    where the reference's Jacobi never converges)."""
     ms = reference_module()
+    budget = 10_000
     if ms is not None:
         from mcreach import CsrMatrix as RefCsr
         rm = RefCsr(m.n, m.rstart, m.col, m.nonzero)
-        cfg = ms.SolverConfig(workers=threads)
-        t0 = time.perf_counter()
-        jr = ms.SOLVERS["jacobi-par"](rm, b, cfg)
-        br = ms.SOLVERS["bicgstab-par"](rm, b, cfg)
-        return time.perf_counter() - t0, "reference", (jr.iterations, br.iterations)
-    from oracle import oracle
-    oracle.set_threads(threads)
-    t0 = time.perf_counter()
-    j = oracle.jacobi(m, b)
-    bb = oracle.bicgstab(m, b)
-    return time.perf_counter() - t0, "port", (j["iterations"], bb["iterations"])
+
+        def run(name, max_it):
+            cfg = ms.SolverConfig(workers=threads, max_iterations=max_it)
+            t0 = time.perf_counter()
+            try:
+                r = ms.SOLVERS[name](rm, b, cfg)
+                it = r.iterations
+            except ms.SolverError as err:
+                it = getattr(getattr(err, "result", None), "iterations", max_it)
+            return time.perf_counter() - t0, it
+        kind = "reference"
+    else:
+        from oracle import oracle
+        oracle.set_threads(threads)
+
+        def run(name, max_it):
+            t0 = time.perf_counter()
+            r = (oracle.jacobi if name.startswith("jacobi") else oracle.bicgstab)(
+                m, b, max_iterations=max_it)
+            return time.perf_counter() - t0, r["iterations"]
+        kind = "port"
+    if jacobi_cap:
+        tj, ij = run("jacobi-par", jacobi_cap)
+        tj *= budget / jacobi_cap
+        ij = budget
+        note = f"jacobi {jacobi_cap} sweeps timed, scaled to the {budget}-sweep budget"
+    else:
+        tj, ij = run("jacobi-par", budget)
+        note = "full solves"
+    tb, ib = run("bicgstab-par", budget)
+    return tj + tb, kind, (ij, ib), note
 
 
 def run_reference_arm(args):
@@ -194,7 +218,7 @@ def run_reference_arm(args):
     kind = None
     iters = None
     for i in range(args.warmup + args.steps):
-        dt, kind, iters = cpu_solve_pair(m, b, threads)
+        dt, kind, iters, note = cpu_solve_pair(m, b, threads, 25 if args.config == "c3" else 0)
         if i >= args.warmup:
             times.append(dt)
     total = sum(times)
@@ -209,7 +233,7 @@ def run_reference_arm(args):
                    "solve_pair": "jacobi-par + bicgstab-par", "parallelism": "cpu threads"},
         "iterations": {"jacobi": iters[0], "bicgstab": iters[1]},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
-                         "sample": f"full C2 solve pair per step ({'mcreach' if kind == 'reference' else 'oracle C port'}, {threads} threads)"},
+                         "sample": f"{args.config.upper()} solve pair per step ({note}; {'mcreach' if kind == 'reference' else 'oracle C port'}, {threads} threads)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -375,10 +399,12 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        dt, kind, iters = cpu_solve_pair(m, b, threads)
+        dt, kind, iters, note = cpu_solve_pair(m, b, threads, 25 if args.config == "c3" else 0)
         cpu = {"value": 2.0 / dt, "unit": UNIT, "cores": threads, "kind": kind,
-               "sample": f"one full C2 solve pair (jacobi {iters[0]} sweeps + bicgstab "
-                         f"{iters[1]} iterations) by {'mcreach jacobi-par/bicgstab-par' if kind == 'reference' else 'the oracle C port'}, {threads} threads, {dt:.1f} s"}
+               "sample": f"one {args.config.upper()} solve pair (jacobi {iters[0]} sweeps + "
+                         f"bicgstab {iters[1]} iterations; {note}) by "
+                         f"{'mcreach jacobi-par/bicgstab-par' if kind == 'reference' else 'the oracle C port'}, "
+                         f"{threads} threads, {dt:.1f} s"}
 
     rj, rb = reps
     jac_it, bic_it = int(rj.iterations), int(rb.iterations)
