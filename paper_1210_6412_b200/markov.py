@@ -30,8 +30,8 @@ from . import _lib
 from .solvers import SolverConfig, SolveResult, _raise_native, outcome
 from .sparse import CsrMatrix
 
-__all__ = ["ChainSystem", "build_system", "reachability_probabilities", "METHODS",
-           "MarkovChainError"]
+__all__ = ["ChainSystem", "build_system", "partition_states", "reachability_probabilities",
+           "METHODS", "MarkovChainError"]
 
 # method name -> (mcr_chain_solve method, reference-order dots)
 METHODS = {"jacobi-gpu": (0, 0), "bicgstab-gpu": (1, 0), "bicgstab-gpu-exact": (1, 1)}
@@ -155,6 +155,21 @@ def _partition(cls: np.ndarray, unc: np.ndarray):
     return kind(prob_one=frozenset(np.flatnonzero(cls == 1).tolist()),
                 prob_zero=frozenset(np.flatnonzero(cls == 0).tolist()),
                 uncertain=unc, index_of={int(s): i for i, s in enumerate(unc)})
+
+
+def partition_states(chain, goals, device: int = 0):
+    """markov.py:184-214 on the device: the StatePartition (prob one / prob zero / uncertain
+    ascending, index_of) -- the reference's type when mcreach is importable."""
+    cs = ChainSystem(chain, goals, device)
+    try:
+        cls = np.empty(cs.n, dtype=np.int8)
+        unc = np.empty(cs.k, dtype=np.int64)
+        rc = cs._L.mcr_chain_export(cs._h, cls.ctypes.data, unc.ctypes.data, None, None, None, None)
+        if rc != _lib.MCR_OK:
+            _raise_native(rc)
+    finally:
+        cs.close()
+    return _partition(cls, unc)
 
 
 def build_system(chain, goals, device: int = 0):

@@ -114,3 +114,15 @@ def test_seeded_guess_chain(gm):
     x1, r1 = gm.reachability_probabilities(ch, goals, "jacobi-gpu", SolverConfig(guess_seed=7))
     assert r1.converged and np.max(np.abs(x1 - x0)) <= 1e-8
     assert r1.iterations != r0.iterations or not np.array_equal(x1, x0)
+
+
+@pytest.mark.parametrize("name", ["demo_g3", "oracle_chain_7", "dtmc_1000"])
+def test_partition_states(gm, name):
+    c = manifest()[name]
+    ch, goals = chain(name)
+    part = gm.partition_states(ch, goals)
+    cls = np.full(ch.n, 2, dtype=np.int8)
+    cls[sorted(part.prob_zero)] = 0
+    cls[sorted(part.prob_one)] = 1
+    assert sha(cls) == c["classes_sha256"] and sha(part.uncertain) == c["uncertain_sha256"]
+    assert all(part.index_of[int(s)] == i for i, s in enumerate(part.uncertain))
