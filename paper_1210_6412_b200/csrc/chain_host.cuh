@@ -42,6 +42,7 @@ static int chain_closure(mcr_chain* c, const unsigned long long* rev_rp, const i
 
 static int chain_build(mcr_chain* c, const int64_t* rstart, const int64_t* col, const double* prob,
                        const int64_t* goals, int64_t ngoals) {
+    NvtxRange range("mcr.chain.build_system");
     const int64_t n = c->n, nnz = c->nnz;
     cudaStream_t s = c->stream;
     TRY(calloc_owned(c, &c->rp, (size_t)n + 1));

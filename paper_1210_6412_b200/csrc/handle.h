@@ -16,6 +16,7 @@
 #include <vector>
 
 #include <cub/device/device_scan.cuh>
+#include <nvtx3/nvToolsExt.h>  // header-only: ranges cost nothing unless a tool attaches
 
 #include "comm.h"
 #include "device.cuh"
@@ -28,6 +29,13 @@ using namespace mcr;
 namespace {
 
 thread_local std::string g_err;
+
+// NVTX range for the lifetime of a scope ("mcr.jacobi", "mcr.create", ...), visible in
+// Nsight Systems / Compute timelines.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 int fail(int code, const std::string& msg) {
     g_err = msg;

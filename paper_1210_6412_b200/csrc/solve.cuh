@@ -75,6 +75,7 @@ void launch_seqdot(mcr_matrix* h, const Vecs& V, int64_t* launches) {
 // the same step (Jacobi: the iterate just written).
 template <int W>
 int exchange_point(mcr_matrix* h, double* buf, int64_t* launches) {
+    NvtxRange range(buf ? "mcr.exchange.allgather+slots" : "mcr.exchange.slots");
     Transport& T = *h->comm;
     const double* send = h->st->send;
     const int rc = buf ? T.allgather_and_slots(buf, (size_t)h->chunk, send, h->recv, SEND_SLOTS,
@@ -160,6 +161,7 @@ int next_batch(int cur) { return std::min(cur * 2, 32); }
 
 int jacobi_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double tol, int64_t max_it,
                 double* d_x_out, mcr_report* rep) {
+    NvtxRange range(h->sharded() ? "mcr.jacobi.shard" : "mcr.jacobi");
     TRY(ensure_work(h));
     long long zero = -1;
     TRY(global_first_zero(h, &zero));
@@ -220,6 +222,7 @@ int jacobi_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double tol
 
 int bicgstab_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double tol,
                   int64_t max_it, double* d_x_out, mcr_report* rep) {
+    NvtxRange range(h->sharded() ? "mcr.bicgstab.shard" : "mcr.bicgstab");
     TRY(ensure_work(h));
     TRY(prepare_inputs(h, d_b, d_x0, V_X));
     set_state(h, tol, max_it);

@@ -36,6 +36,7 @@ int build_sell(mcr_matrix* h, bool offdiag, mcr_matrix::SellDev* S) {
 
 int ensure_offdiag(mcr_matrix* h) {
     if (h->r_ready || h->storage != MCR_STORAGE_CSR) return MCR_OK;
+    NvtxRange range("mcr.without_diagonal");
     if (h->use_sell) {
         TRY(build_sell(h, true, &h->rsell));
         h->r_ready = true;
@@ -136,6 +137,7 @@ int alloc_csr(mcr_matrix* h, int64_t n, int64_t nnz) {
 
 int create_impl(mcr_matrix* h, int64_t n, const int64_t* rs, const int64_t* col,
                 const double* val, int storage) {
+    NvtxRange range("mcr.create");
     TRY(init_handle(h));
     if (n == 0) return MCR_OK;
     const int64_t nnz = rs[n];
