@@ -35,6 +35,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "time-to-solution & SpMV HBM GB/s (Jacobi/BiCGStab) at 1/2/4/8 B200 vs CPU"
 UNIT = "solves/s"
+STORAGES = {"auto": 0, "tiles": 5, "staged": 6}  # C5 layouts (include/mcr.h MCR_STORAGE_*)
 FALLBACK_HBM_GBS = 6650.0
 
 
@@ -497,12 +498,12 @@ def run_c5(args):
     t_gen = time.perf_counter()
     if world > 1:
         comm = Comm.nccl(local)
-        h = ShardMatrix.generated(comm, n, mean, 1, 10, seed)
+        h = ShardMatrix.generated(comm, n, mean, 1, 10, seed, storage=STORAGES[args.storage])
         if args.p2p:
             h.enable_p2p()
     else:
         comm = None
-        h = DeviceMatrix.generated(n, mean, 1, 10, seed, device=local, storage=_lib.STORAGE_TILES)
+        h = DeviceMatrix.generated(n, mean, 1, 10, seed, device=local, storage=STORAGES[args.storage])
     info = h.info()
     rows, nnz_local = int(info["n"]), int(info["nnz"])
     stream = torch.cuda.Stream(dev)
@@ -647,6 +648,8 @@ def main():
     ap.add_argument("--p2p", action="store_true",
                     help="C5 at N > 1: fused exchange (producers store into peers' copies)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--storage", default="auto", choices=sorted(STORAGES),
+                    help="C5 layout: auto (band-staged at this size), tiles or staged")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)

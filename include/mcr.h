@@ -51,19 +51,22 @@ enum {
 enum { MCR_BD_NONE = 0, MCR_BD_Y_PREV_W = 1, MCR_BD_Q_V = 2, MCR_BD_T_T = 3 };
 
 /* Device storage selection for mcr_matrix_create. AUTO picks dense 32-row slabs when the
- * matrix is at least 2/3 full and n >= 1024; otherwise CSR, laid out as SELL-32-sigma when the
- * caller asks for it (coalesced thread-per-row streaming) and as CSR tiles staged by
- * TMA bulk copies otherwise (the default). SELL / TILES force one CSR layout. Tiled systems
- * whose tiles all fit on the GPU at once (<= 2 tiles per SM) solve in ONE cooperative launch
- * (grid barriers between sweeps); TILES_STREAM opts out of that. mcr_matrix_info reports the
- * layout in use (DENSE, SELL or TILES). */
+ * matrix is at least 2/3 full and n >= 1024; the band-staged two-pass layout (STAGED) when
+ * the gathered vector is far larger than L2 (8 * n >= 80 MB, rows of at most 2048 entries,
+ * fewer than 2^31 entries); otherwise CSR, laid out as SELL-32-sigma when the caller asks for
+ * it (coalesced thread-per-row streaming) and as CSR tiles staged by TMA bulk copies otherwise
+ * (the default). SELL / TILES / STAGED force one layout (STAGED falls back to TILES when the
+ * matrix is not eligible). Tiled systems whose tiles all fit on the GPU at once (<= 2 tiles
+ * per SM) solve in ONE cooperative launch (grid barriers between sweeps); TILES_STREAM opts
+ * out of that. mcr_matrix_info reports the layout in use (DENSE, SELL, TILES or STAGED). */
 enum {
     MCR_STORAGE_AUTO = 0,
     MCR_STORAGE_CSR = 1,
     MCR_STORAGE_DENSE = 2,
     MCR_STORAGE_SELL = 3,
     MCR_STORAGE_TILES = 4,
-    MCR_STORAGE_TILES_STREAM = 5 /* tiles, but never the single-launch small-system solvers */
+    MCR_STORAGE_TILES_STREAM = 5, /* tiles, but never the single-launch small-system solvers */
+    MCR_STORAGE_STAGED = 6        /* column bands: products pass + row-sum pass (staged.cuh) */
 };
 
 typedef struct mcr_matrix mcr_matrix;
@@ -83,7 +86,7 @@ typedef struct mcr_report {
 typedef struct mcr_matrix_info {
     int64_t n;
     int64_t nnz;
-    int32_t storage;             /* MCR_STORAGE_DENSE, MCR_STORAGE_SELL or MCR_STORAGE_TILES */
+    int32_t storage;             /* MCR_STORAGE_DENSE, _SELL, _TILES or _STAGED               */
     int32_t device;
     int64_t tiles;               /* CSR row tiles                                           */
     int64_t max_row_nnz;

@@ -21,6 +21,7 @@ MCR_CUDA_ERROR = 5
 MCR_INVALID_ARGUMENT = 6
 
 STORAGE_AUTO, STORAGE_CSR, STORAGE_DENSE, STORAGE_SELL, STORAGE_TILES, STORAGE_TILES_STREAM = 0, 1, 2, 3, 4, 5
+STORAGE_STAGED = 6
 BREAKDOWN_NAMES = {1: "y_prev*w", 2: "q*v", 3: "t*t"}
 
 EXPORTS = (

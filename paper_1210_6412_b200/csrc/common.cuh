@@ -63,6 +63,7 @@ struct SolveState {
     unsigned long long maxbits;  // atomicMax of |.| bit patterns (non-negative doubles order as u64)
     unsigned int done;           // last-CTA counter
     unsigned int tile_ctr;       // dynamic tile scheduler of k_spmv
+    unsigned long long p1_ctr;   // chunk tickets of the staged products pass (staged.cuh)
     double y, a, w, beta, qv, tt, ts, resid;
     int small;
     int seqdots;  // 1: inner products by k_seqdot (reference order, bit-exact), not the tree

@@ -6,6 +6,7 @@
 //   vector.cuh   BiCGStab vector phases, reference-order dots, row-shard finalisation
 //   dense.cuh    dense slab GEMV (k_dense<EPI>)
 //   upload.cuh   upload-time kernels
+//   staged.cuh   band-staged two-pass SpMV for x far larger than L2
 #pragma once
 
 #include "common.cuh"
@@ -14,3 +15,4 @@
 #include "vector.cuh"
 #include "dense.cuh"
 #include "upload.cuh"
+#include "staged.cuh"

@@ -9,6 +9,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -141,6 +142,18 @@ struct mcr_matrix {
         long long slots = 0;
     } sell, rsell;
     bool use_sell = false;
+    // band-staged copy (staged.cuh): systems whose x is far larger than L2
+    struct StagedDev {
+        double* pval = nullptr;
+        int* pcol = nullptr;
+        unsigned short* lidx = nullptr;
+        double* prod = nullptr;
+        unsigned long long* seg = nullptr;
+        long long npos = 0;
+        int nb = 0, band = 0;
+        int p1_grid = 1, grid = 1;  // pass-1 / pass-2 CTAs
+    } stg;
+    bool use_staged = false;
     // dense slabs
     double* dense = nullptr;
     int nslabs = 0;
@@ -222,6 +235,11 @@ int keep_pool_memory(int device) {
 
 Csr csr_full(const mcr_matrix* h) {
     return Csr{h->rp, h->col, h->val, h->desc, h->ntiles, (int)h->n};
+}
+Staged staged_view(const mcr_matrix* h) {
+    const auto& S = h->stg;
+    static const int early = std::getenv("MCR_STAGED_PDL") ? std::atoi(std::getenv("MCR_STAGED_PDL")) : 0;
+    return Staged{h->rp, S.lidx, S.seg, S.pval, S.pcol, S.prod, h->desc, S.npos, h->ntiles, S.nb, early};
 }
 Csr csr_off(const mcr_matrix* h) {
     return Csr{h->rrp, h->rcol, h->rval, h->rdesc, h->ntiles, (int)h->n};

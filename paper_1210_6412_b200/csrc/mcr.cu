@@ -44,7 +44,8 @@ MCR_API void mcr_matrix_destroy(mcr_matrix* h) {
                             h->rrp, h->rcol, h->rval, h->dense, h->d, h->work, h->P, h->st,
                             h->sell.sptr, h->sell.perm, h->sell.col, h->sell.val, h->sell.swidth,
                             h->rsell.sptr, h->rsell.perm, h->rsell.col, h->rsell.val,
-                            h->rsell.swidth, h->maxslot, h->recv};
+                            h->rsell.swidth, h->maxslot, h->recv, h->stg.pval, h->stg.pcol,
+                            h->stg.lidx, h->stg.prod, h->stg.seg};
             for (void* p : ptrs)
                 if (p) cudaFreeAsync(p, s);
             cudaStreamSynchronize(s);
@@ -171,7 +172,7 @@ MCR_API int mcr_shard_create(mcr_comm* comm, int64_t n_global, int64_t row0, int
     if (rows < 1) return fail(MCR_DIMENSION, "every rank needs at least one row (n >= world)");
     TRY(check_csr(rows, rstart, col, nonzero));
     const int64_t chunk = (n_global + T.world - 1) / T.world;
-    return create_handle(rows, rstart, col, nonzero, T.device, MCR_STORAGE_TILES_STREAM, comm->t,
+    return create_handle(rows, rstart, col, nonzero, T.device, MCR_STORAGE_AUTO, comm->t,
                          n_global, row0, chunk, out);
 }
 
@@ -258,8 +259,7 @@ MCR_API int mcr_generate(mcr_comm* comm, int device, int64_t n_global, double me
     if (comm) {
         h->comm = comm->t;
         h->world = world;
-        h->rank = rank;
-        storage = MCR_STORAGE_TILES_STREAM;
+        h->rank = rank;  // (shards never take the dense or single-launch paths)
     }
     GenParams P{};
     P.seed = seed;
@@ -457,7 +457,9 @@ MCR_API int mcr_matrix_info_get(const mcr_matrix* h, mcr_matrix_info* info) {
     info->n = h->n;
     info->nnz = h->nnz;
     info->storage = h->storage == MCR_STORAGE_DENSE ? MCR_STORAGE_DENSE
-                    : (h->use_sell ? MCR_STORAGE_SELL : MCR_STORAGE_TILES);
+                    : h->use_sell                    ? MCR_STORAGE_SELL
+                    : h->use_staged                  ? MCR_STORAGE_STAGED
+                                                     : MCR_STORAGE_TILES;
     info->device = h->device;
     info->tiles = h->ntiles;
     info->max_row_nnz = h->max_row;

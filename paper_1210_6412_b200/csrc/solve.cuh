@@ -31,11 +31,12 @@ void launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t sm
     cfg.blockDim = dim3(block);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
+    static const bool pdl = std::getenv("MCR_NO_PDL") == nullptr;  // A/B switch for profiling
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl ? 1 : 0;
     cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
@@ -44,6 +45,11 @@ void launch_mv(mcr_matrix* h, bool offdiag, const double* x, const Vecs& V, int6
     if (h->storage == MCR_STORAGE_DENSE) {
         launch_pdl(k_dense<EPI>, h->nslabs, 32, DENSE_SMEM, h->stream, (const double*)h->dense,
                    (int)h->n, (int)((h->n + 1) & ~1ll), x, V, h->st);
+    } else if (h->use_staged) {  // products pass, then the row sums (Jacobi skips the diagonal)
+        const Staged A = staged_view(h);
+        launch_pdl(k_stage_products<EPI>, h->stg.p1_grid, STG_P1_NT, 0, h->stream, A, x, V, h->st);
+        launch_pdl(k_spmv_staged<EPI>, h->stg.grid, SP_THREADS, STG_SMEM, h->stream, A, V, h->st);
+        ++*launches;
     } else if (h->use_sell) {
         const auto& S = offdiag ? h->rsell : h->sell;
         launch_pdl(k_sell<EPI>, S.nwin * (SELL_W / SELL_CTA), SELL_CTA, 0, h->stream,

@@ -35,7 +35,8 @@ int build_sell(mcr_matrix* h, bool offdiag, mcr_matrix::SellDev* S) {
 }
 
 int ensure_offdiag(mcr_matrix* h) {
-    if (h->r_ready || h->storage != MCR_STORAGE_CSR) return MCR_OK;
+    // the staged layout flags the diagonal instead of keeping a second copy
+    if (h->r_ready || h->storage != MCR_STORAGE_CSR || h->use_staged) return MCR_OK;
     NvtxRange range("mcr.without_diagonal");
     if (h->use_sell) {
         TRY(build_sell(h, true, &h->rsell));
@@ -67,6 +68,69 @@ int ensure_offdiag(mcr_matrix* h) {
                                                                      h->rdesc);
     CK(cudaGetLastError());
     h->r_ready = true;
+    return MCR_OK;
+}
+
+// Band-staged copy (staged.cuh): segment counts per (band, tile), scan, placement. Leaves
+// use_staged false when the staged positions would not fit the 32-bit segment offsets.
+constexpr double STAGED_AUTO_X_BYTES = 80e6;  // x this large (n >= 1e7): AUTO stages
+constexpr int STAGED_AUTO_BAND = 4 << 20;                   // columns per band (32 MB of x)
+
+int build_staged(mcr_matrix* h, bool forced) {
+    NvtxRange range("mcr.stage");
+    auto& S = h->stg;
+    const int64_t nfull = h->n_full();
+    long long band = forced ? (nfull + 7) / 8 : STAGED_AUTO_BAND;
+    if (const char* env = std::getenv("MCR_STAGED_BAND")) band = std::max(1ll, std::atoll(env));
+    band = std::max(band, (long long)((nfull + STG_NB_MAX - 1) / STG_NB_MAX));
+    band = std::max(band, 1ll);
+    S.band = (int)band;
+    S.nb = (int)((nfull + band - 1) / band);
+    const int nt = h->ntiles;
+    const size_t K = (size_t)S.nb * (size_t)nt;
+    long long* counts = nullptr;
+    long long* offs = nullptr;
+    CK(cudaMallocAsync((void**)&counts, sizeof(long long) * (K + 1), h->stream));
+    CK(cudaMallocAsync((void**)&offs, sizeof(long long) * (K + 1), h->stream));
+    CK(cudaMemsetAsync(counts + K, 0, sizeof(long long), h->stream));
+    const int blocks = (nt + STG_BUILD_WARPS - 1) / STG_BUILD_WARPS;
+    k_stage_count<<<blocks, STG_BUILD_WARPS * 32, 0, h->stream>>>(h->col, h->desc, nt, S.band,
+                                                                   S.nb, counts);
+    CK(cudaGetLastError());
+    size_t tmp = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, counts, offs, K + 1, h->stream));
+    void* dtmp = nullptr;
+    CK(cudaMallocAsync(&dtmp, tmp, h->stream));
+    CK(cub::DeviceScan::ExclusiveSum(dtmp, tmp, counts, offs, K + 1, h->stream));
+    CK(cudaFreeAsync(dtmp, h->stream));
+    CK(cudaFreeAsync(counts, h->stream));
+    long long npos = 0;
+    CK(cudaMemcpyAsync(&npos, offs + K, sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    if (npos >= (1ll << 32)) {
+        CK(cudaFreeAsync(offs, h->stream));
+        return MCR_OK;
+    }
+    S.npos = npos;
+    TRY(dalloc(h, &S.pval, (size_t)npos));
+    TRY(dalloc(h, &S.pcol, (size_t)npos));
+    TRY(dalloc(h, &S.prod, (size_t)npos));
+    TRY(dalloc(h, &S.lidx, (size_t)h->nnz + 16));
+    TRY(dalloc(h, &S.seg, K));
+    k_stage_fill<<<blocks, STG_BUILD_WARPS * 32, 0, h->stream>>>(
+        h->rp, h->col, h->val, h->desc, nt, S.band, S.nb, (long long)h->roff, offs, S.pval, S.pcol,
+        S.lidx, S.seg);
+    CK(cudaGetLastError());
+    CK(cudaFreeAsync(offs, h->stream));
+    int sms = 0, per_sm = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv_staged<EPI_V>, SP_THREADS,
+                                                     STG_SMEM));
+    S.grid = std::max(1, std::min(nt, sms * std::max(per_sm, 1)));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stage_products<EPI_V>, STG_P1_NT, 0));
+    S.p1_grid = (int)std::max<long long>(1, std::min<long long>((npos / 2 + STG_P1_NT - 1) / STG_P1_NT,
+                                                                (long long)sms * std::max(per_sm, 1)));
+    h->use_staged = true;
     return MCR_OK;
 }
 
@@ -106,6 +170,13 @@ static int set_kernel_attributes() {
     CK(cudaFuncSetAttribute(k_spmv<EPI_S0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sp));
     CK(cudaFuncSetAttribute(k_spmv<EPI_V>, cudaFuncAttributeMaxDynamicSharedMemorySize, sp));
     CK(cudaFuncSetAttribute(k_spmv<EPI_T>, cudaFuncAttributeMaxDynamicSharedMemorySize, sp));
+    const int sg = (int)STG_SMEM;
+    CK(cudaFuncSetAttribute(k_spmv_staged<EPI_Y>, cudaFuncAttributeMaxDynamicSharedMemorySize, sg));
+    CK(cudaFuncSetAttribute(k_spmv_staged<EPI_RESID>, cudaFuncAttributeMaxDynamicSharedMemorySize, sg));
+    CK(cudaFuncSetAttribute(k_spmv_staged<EPI_JACOBI>, cudaFuncAttributeMaxDynamicSharedMemorySize, sg));
+    CK(cudaFuncSetAttribute(k_spmv_staged<EPI_S0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sg));
+    CK(cudaFuncSetAttribute(k_spmv_staged<EPI_V>, cudaFuncAttributeMaxDynamicSharedMemorySize, sg));
+    CK(cudaFuncSetAttribute(k_spmv_staged<EPI_T>, cudaFuncAttributeMaxDynamicSharedMemorySize, sg));
     return MCR_OK;
 }
 
@@ -305,12 +376,18 @@ int finish_create(mcr_matrix* h, int64_t n, const int64_t* rs, int storage,
         CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv<EPI_V>, SP_THREADS, SP_SMEM));
         h->spmv_grid = std::max(1, std::min(h->ntiles, sms * std::max(per_sm, 1)));
+        double auto_bytes = STAGED_AUTO_X_BYTES;  // tuning / test override of the AUTO cut
+        if (const char* env = std::getenv("MCR_STAGED_MIN_X_BYTES")) auto_bytes = std::atof(env);
+        const bool stage = !h->use_sell && h->nnz > 0 && h->max_row <= TILE_NNZ &&
+                           (storage == MCR_STORAGE_STAGED ||
+                            (storage == MCR_STORAGE_AUTO &&
+                             8.0 * (double)h->n_full() >= auto_bytes));
         int pj = 0, pb = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pj, k_jacobi_small, SM_NT, 0));
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pb, k_bicg_small, SM_NT, 0));
         const int coresident = sms * std::min(pj, pb);
         // one tile per CTA keeps the per-sweep critical path to a single tile
-        if (!h->use_sell && !h->sharded() && storage != MCR_STORAGE_TILES_STREAM &&
+        if (!h->use_sell && !h->sharded() && !stage && storage != MCR_STORAGE_TILES_STREAM &&
             h->ntiles <= coresident && h->ntiles <= 2 * sms)
             h->small_grid = h->ntiles;
         TRY(dalloc(h, &h->maxslot, 3));
@@ -324,6 +401,7 @@ int finish_create(mcr_matrix* h, int64_t n, const int64_t* rs, int storage,
         TRY(dalloc(h, &h->desc, desc.size()));
         CK(cudaMemcpyAsync(h->desc, desc.data(), sizeof(TileDesc) * desc.size(),
                            cudaMemcpyHostToDevice, h->stream));
+        if (stage) TRY(build_staged(h, storage == MCR_STORAGE_STAGED));
         CK(cudaStreamSynchronize(h->stream));
     }
     h->first_zero = h->fz_host == ~0ull ? -1 : (long long)h->fz_host + h->roff;  // global row

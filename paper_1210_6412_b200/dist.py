@@ -144,12 +144,12 @@ class ShardMatrix:
 
     @classmethod
     def generated(cls, comm: Comm, n: int, mean_offdiag: float = 7.0, lo: int = 1, hi: int = 10,
-                  seed: int = 0) -> "ShardMatrix":
+                  seed: int = 0, storage: int = _lib.STORAGE_AUTO) -> "ShardMatrix":
         """This rank's rows of the row-keyed synthetic system, generated in HBM (config C5)."""
         L = _lib.load()
         h = ctypes.c_void_p()
         rc = L.mcr_generate(comm.handle, comm.device, int(n), float(mean_offdiag), int(lo),
-                            int(hi), int(seed), _lib.STORAGE_TILES_STREAM, ctypes.byref(h))
+                            int(hi), int(seed), int(storage), ctypes.byref(h))
         if rc != _lib.MCR_OK:
             _raise_native(rc)
         row0, rows = shard_rows(int(n), comm.world, comm.rank)

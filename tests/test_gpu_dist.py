@@ -199,6 +199,33 @@ def test_fused_p2p_bit_identical_to_allgather(mods):
 
 
 @pytest.mark.slow
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("name", P2P_CASES)
+@pytest.mark.parametrize("method", ["jacobi", "bicgstab"])
+def test_sharded_staged(mods, name, world, method, monkeypatch):
+    """Row shards in the band-staged layout (AUTO picks it once x is large; the cut is lowered
+    to 0 here): the same results as the tiled shards and the reference."""
+    monkeypatch.setenv("MCR_STAGED_MIN_X_BYTES", "0")
+    check(mods, method, name, world)
+    check(mods, method, name, world, p2p=True)
+
+
+def test_sharded_staged_layout_in_use(mods, monkeypatch):
+    dist, _ = mods
+    m, _ = system("c1_seed77")
+    monkeypatch.setenv("MCR_STAGED_MIN_X_BYTES", "0")
+    comms = dist.Comm.local_group(2)
+    try:
+        sh = dist.ShardMatrix.from_matrix(comms[1], m)
+        try:
+            assert sh.info()["storage"] == 6
+        finally:
+            sh.close()
+    finally:
+        for c in comms:
+            c.close()
+
+
 def test_fused_p2p_c2(mods):
     check(mods, "jacobi", "c2_trial0", 4, p2p=True)
     check(mods, "bicgstab", "c2_trial0", 4, iter_slack=6, p2p=True)

@@ -121,15 +121,16 @@ def test_c2_bicgstab_tree_dots(gs):
 @pytest.mark.parametrize("name", ["kat_golden2x2", "kat_identity4", "kat_divergent",
                                   "grid_20_9", "grid_50_5", "dense_1024", "c1_seed77",
                                   "chain_random2", "c4_7647_15293", "seeded_guess"])
-@pytest.mark.parametrize("storage", [2, 3, 4, 5])
+@pytest.mark.parametrize("storage", [2, 3, 4, 5, 6])
 def test_forced_storage_matches_reference(gs, name, storage):
-    """Dense slabs (2), SELL-32-sigma (3), CSR tiles solved in one cooperative launch (4) and
-    CSR tiles through the per-iteration TMA-pipelined kernels (5) give the same bits."""
+    """Dense slabs (2), SELL-32-sigma (3), CSR tiles solved in one cooperative launch (4),
+    CSR tiles through the per-iteration TMA-pipelined kernels (5) and the band-staged two-pass
+    SpMV (6; forced, the columns split into up to 8 bands) give the same bits."""
     from paper_1210_6412_b200._lib import MCR_OK, MCR_NOT_CONVERGED
     m, b = system(name)
     dm = gs.DeviceMatrix(m, 0, storage)
     try:
-        assert dm.info()["storage"] == min(storage, 4)
+        assert dm.info()["storage"] == (6 if storage == 6 else min(storage, 4))
         def x0(cfg):
             g = cfg["guess_seed"]
             return None if g is None else np.random.default_rng(g).random(m.n)
@@ -161,6 +162,58 @@ def test_forced_storage_matches_reference(gs, name, storage):
         xr = np.random.default_rng(7).uniform(-3, 3, m.n)
         assert np.array_equal(dm.matvec(xr), oracle.spmv(m, xr))
         assert dm.residual_inf(xr, b) == oracle.residual_inf(m, xr, b)
+    finally:
+        dm.close()
+
+
+def test_staged_c2_bit_identical(gs):
+    """The band-staged layout on C2 (8 bands of 125 000 columns): Jacobi bit-identical to the
+    reference, SpMV and residual bit-identical to the oracle."""
+    from oracle import oracle
+    from paper_1210_6412_b200._lib import MCR_OK
+    m, b = system("c2_trial0")
+    dm = gs.DeviceMatrix(m, 0, 6)
+    try:
+        assert dm.info()["storage"] == 6
+        exp = expected("c2_trial0", "jacobi")  # C2 fixtures keep a hash + a strided sample
+        rc, x, rep = dm.solve("jacobi", b, None, 1e-10, 10_000)
+        assert rc == MCR_OK and rep.iterations == exp["iterations"]
+        assert sha(x) == exp["x_sha256"]
+        assert float(rep.residual_inf).hex() == exp["residual_inf"]
+        xr = np.random.default_rng(11).uniform(-3, 3, m.n)
+        assert np.array_equal(dm.matvec(xr), oracle.spmv(m, xr))
+        exp = expected("c2_trial0", "bicgstab")
+        rc, x, rep = dm.solve("bicgstab", b, None, 1e-10, 10_000, dots="sequential")
+        assert rc == MCR_OK and rep.iterations == exp["iterations"]
+        assert sha(x) == exp["x_sha256"]
+    finally:
+        dm.close()
+
+
+def test_staged_band_sizes(gs, monkeypatch):
+    """Any band width gives the same bits: one column per band up to one band for all."""
+    from oracle import oracle
+    from paper_1210_6412_b200.generator import GenSpec, generate_dd_matrix
+    m = generate_dd_matrix(GenSpec(n=3000, nnz=30_000, seed=21))
+    xr = np.random.default_rng(5).uniform(-2, 2, m.n)
+    want = oracle.spmv(m, xr)
+    for band in (1, 7, 24, 100, 2999, 3000, 10**6):
+        monkeypatch.setenv("MCR_STAGED_BAND", str(band))
+        dm = gs.DeviceMatrix(m, 0, 6)
+        try:
+            assert dm.info()["storage"] == 6
+            assert np.array_equal(dm.matvec(xr), want)
+        finally:
+            dm.close()
+
+
+def test_staged_falls_back_for_long_rows(gs):
+    """Rows longer than one tile (2048 entries) are not staged: forced STAGED reports TILES."""
+    from paper_1210_6412_b200.generator import GenSpec, generate_dd_matrix
+    m = generate_dd_matrix(GenSpec(n=2500, density=0.9, seed=3))  # rows ~2250 entries
+    dm = gs.DeviceMatrix(m, 0, 6)
+    try:
+        assert dm.info()["storage"] == 4
     finally:
         dm.close()
 

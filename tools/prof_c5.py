@@ -9,6 +9,7 @@ storages = [int(s) for s in sys.argv[2:]] or [0]
 L = _lib.load()
 x = torch.rand(n, dtype=torch.float64, device="cuda"); y = torch.empty_like(x)
 stream = torch.cuda.Stream(); torch.cuda.set_stream(stream)
+y0 = None
 for st in storages:
     dm = DeviceMatrix.generated(n, 7.0, 1, 10, 2024, storage=st)
     L.mcr_set_stream(dm.handle, ctypes.c_void_p(stream.cuda_stream))
@@ -20,5 +21,10 @@ for st in storages:
         torch.cuda.synchronize(); ts.append(e0.elapsed_time(e1))
     t = sorted(ts)[2] * 1e-3
     alg = 12 * inf["nnz"] + 8 * (n + 1) + 16 * n
-    print(f"n={n} storage={inf['storage']} nnz={inf['nnz']} bytes={inf['device_bytes']/1e9:.1f}GB spmv {t*1e3:.3f} ms {alg/t/1e9:.0f} GB/s alg", flush=True)
+    same = ""
+    if y0 is None:
+        y0 = y.clone()
+    else:
+        same = f" bit-identical to the first: {bool(torch.equal(y, y0))}"
+    print(f"n={n} storage={inf['storage']} band={os.environ.get('MCR_STAGED_BAND', 'auto')} nnz={inf['nnz']} bytes={inf['device_bytes']/1e9:.1f}GB spmv {t*1e3:.3f} ms {alg/t/1e9:.0f} GB/s alg{same}", flush=True)
     dm.close()
