@@ -620,7 +620,10 @@ def run_c5(args):
         "time_to_solution_ms": {"jacobi": rj.device_seconds * 1e3, "bicgstab": rb.device_seconds * 1e3},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": None,
-                     "kernel": "k_spmv<EPI_Y> on this rank's rows",
+                     "kernel": ("k_stage_products + k_spmv_staged (band-staged SpMV, both passes)"
+                                if info["storage"] == _lib.STORAGE_STAGED else "k_spmv<EPI_Y>")
+                               + " on this rank's rows",
+                     "storage": {0: "auto", 4: "tiles", 5: "tiles", 6: "staged"}.get(info["storage"], str(info["storage"])),
                      "algorithmic_bytes": alg, "launch_us": spmv_s * 1e6, "peak_source": peak_src},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 2 * 8 * rows,
                 "d2h_bytes_per_step": 2 * 8 * rows,
