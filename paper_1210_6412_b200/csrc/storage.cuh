@@ -80,7 +80,8 @@ int build_staged(mcr_matrix* h, bool forced) {
     NvtxRange range("mcr.stage");
     auto& S = h->stg;
     const int64_t nfull = h->n_full();
-    long long band = forced ? (nfull + 7) / 8 : STAGED_AUTO_BAND;
+    // forced on a small system: up to 8 bands, so the multi-band path is exercised
+    long long band = forced ? std::min<long long>((nfull + 7) / 8, STAGED_AUTO_BAND) : STAGED_AUTO_BAND;
     if (const char* env = std::getenv("MCR_STAGED_BAND")) band = std::max(1ll, std::atoll(env));
     band = std::max(band, (long long)((nfull + STG_NB_MAX - 1) / STG_NB_MAX));
     band = std::max(band, 1ll);
