@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <climits>
 #include <cmath>
 #include <cstdio>
@@ -36,6 +37,17 @@ thread_local std::string g_err;
 struct NvtxRange {
     explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
     ~NvtxRange() { nvtxRangePop(); }
+};
+
+// MCR_TRACE=1: host timestamps of the create / solve stages on stderr (profiling aid).
+struct Trace {
+    bool on = std::getenv("MCR_TRACE") != nullptr;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    void mark(const char* what) {
+        if (!on) return;
+        const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        std::fprintf(stderr, "[mcr] %-28s %8.3f ms\n", what, ms);
+    }
 };
 
 int fail(int code, const std::string& msg) {
@@ -160,7 +172,9 @@ struct mcr_matrix {
     // diagonal + facts
     double* d = nullptr;
     long long first_zero = -1;
-    unsigned long long fz_host = ~0ull;  // D2H target of the first-zero-diagonal search
+    unsigned long long fz_host[2] = {~0ull, 0ull};  // D2H target: first zero-diagonal row,
+                                                    // count of stored diagonal entries
+    int64_t nnz_off = 0;                            // entries of Jacobi's off-diagonal copy
     int bad_host[2] = {0, 0};            // D2H target of the upload checks
     long long max_row = 0;
     // workspace

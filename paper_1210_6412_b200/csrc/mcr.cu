@@ -64,7 +64,7 @@ MCR_API int mcr_matrix_create(int64_t n, const int64_t* rstart, const int64_t* c
                               const double* nonzero, int device, int storage, mcr_matrix** out) {
     if (!out) return fail(MCR_INVALID_ARGUMENT, "out is NULL");
     *out = nullptr;
-    TRY(check_csr(n, rstart, col, nonzero));
+    TRY(check_csr(n, rstart, col, nonzero, false));  // monotonicity: checked during the upload
     return create_handle(n, rstart, col, nonzero, device, storage, nullptr, n, 0, n, out);
 }
 
@@ -170,7 +170,7 @@ MCR_API int mcr_shard_create(mcr_comm* comm, int64_t n_global, int64_t row0, int
                                        " must hold rows [" + std::to_string(want0) + ", " +
                                        std::to_string(want0 + want) + ")");
     if (rows < 1) return fail(MCR_DIMENSION, "every rank needs at least one row (n >= world)");
-    TRY(check_csr(rows, rstart, col, nonzero));
+    TRY(check_csr(rows, rstart, col, nonzero, false));
     const int64_t chunk = (n_global + T.world - 1) / T.world;
     return create_handle(rows, rstart, col, nonzero, T.device, MCR_STORAGE_AUTO, comm->t,
                          n_global, row0, chunk, out);

@@ -168,6 +168,7 @@ int next_batch(int cur) { return std::min(cur * 2, 32); }
 int jacobi_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double tol, int64_t max_it,
                 double* d_x_out, mcr_report* rep) {
     NvtxRange range(h->sharded() ? "mcr.jacobi.shard" : "mcr.jacobi");
+    Trace tr;
     TRY(ensure_work(h));
     long long zero = -1;
     TRY(global_first_zero(h, &zero));
@@ -176,6 +177,7 @@ int jacobi_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double tol
         return fail(MCR_ZERO_DIAGONAL, "zero diagonal entry in row " + std::to_string(zero));
     }
     TRY(ensure_offdiag(h));
+    tr.mark("jacobi: off-diagonal ready");
     TRY(prepare_inputs(h, d_b, d_x0, V_X));
     set_state(h, tol, max_it);
     CK(cudaMemcpyAsync(h->st, h->h_st, sizeof(SolveState), cudaMemcpyHostToDevice, h->stream));
@@ -217,6 +219,7 @@ int jacobi_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double tol
         CK(cudaMemcpyAsync(d_x_out, x + h->roff, sizeof(double) * (size_t)h->n,
                            cudaMemcpyDeviceToDevice, h->stream));
     CK(cudaStreamSynchronize(h->stream));
+    tr.mark("jacobi: done");
     const SolveState& s = *h->h_st;
     rep->iterations = s.it;
     rep->converged = s.stop == CONVERGED;

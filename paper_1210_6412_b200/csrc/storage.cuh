@@ -51,9 +51,7 @@ int ensure_offdiag(mcr_matrix* h) {
     CK(cudaMallocAsync(&dtmp, tmp, h->stream));
     CK(cub::DeviceScan::ExclusiveSum(dtmp, tmp, h->offlen, h->rrp, n + 1, h->stream));
     CK(cudaFreeAsync(dtmp, h->stream));
-    long long roff = 0;
-    CK(cudaMemcpyAsync(&roff, h->rrp + n, sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
-    CK(cudaStreamSynchronize(h->stream));
+    const int64_t roff = h->nnz_off;  // counted at create: no read-back, no synchronisation
     TRY(dalloc(h, &h->rcol, (size_t)roff + CSR_PAD));
     TRY(dalloc(h, &h->rval, (size_t)roff + CSR_PAD));
     const int threads = 256;
@@ -137,17 +135,20 @@ int build_staged(mcr_matrix* h, bool forced) {
 
 // Greedy tiles: consecutive rows while rows <= TILE_ROWS and entries <= TILE_NNZ; a row with
 // more than TILE_NNZ entries is a tile of its own.
-std::vector<int> make_tiles(int64_t n, const int64_t* rs, long long* max_row) {
+std::vector<int> make_tiles(int64_t n, const int64_t* rs, long long* max_row,
+                            bool* monotone = nullptr) {
     std::vector<int> t;
     t.reserve((size_t)(n / 64 + 2));
     t.push_back(0);
     long long mr = 0;
     int64_t r = 0;
+    bool mono = true;
     while (r < n) {
         const int64_t start = r;
         int64_t nnz = 0;
         while (r < n && r - start < TILE_ROWS) {
             const int64_t len = rs[r + 1] - rs[r];
+            mono &= len >= 0;
             mr = std::max<long long>(mr, len);
             if (nnz + len > TILE_NNZ && r > start) break;
             nnz += len;
@@ -156,6 +157,7 @@ std::vector<int> make_tiles(int64_t n, const int64_t* rs, long long* max_row) {
         }
         t.push_back((int)r);
     }
+    if (monotone) *monotone = mono;
     *max_row = mr;
     return t;
 }
@@ -210,8 +212,10 @@ int alloc_csr(mcr_matrix* h, int64_t n, int64_t nnz) {
 int create_impl(mcr_matrix* h, int64_t n, const int64_t* rs, const int64_t* col,
                 const double* val, int storage) {
     NvtxRange range("mcr.create");
+    Trace tr;
     TRY(init_handle(h));
     if (n == 0) return MCR_OK;
+    tr.mark("create: handle");
     const int64_t nnz = rs[n];
     TRY(alloc_csr(h, n, nnz));
     CK(cudaMemcpyAsync(h->rp, rs, sizeof(long long) * (size_t)(n + 1), cudaMemcpyHostToDevice,
@@ -233,18 +237,26 @@ int create_impl(mcr_matrix* h, int64_t n, const int64_t* rs, const int64_t* col,
         k_col64to32<<<(int)std::min<int64_t>((nnz + 255) / 256, 1 << 16), 256, 0, h->stream>>>(
             tmp, h->col, nnz, (int)h->n_global, bad);
         k_check_rows<<<(int)std::min<int64_t>((n + 255) / 256, 1 << 16), 256, 0, h->stream>>>(
-            h->rp, h->col, (int)n, bad + 1);
+            h->rp, h->col, (int)n, (long long)nnz, bad + 1);
     }
     CK(cudaGetLastError());
+    // the row tiles are cut on the host while the copies are in flight -- before the D2H of the
+    // check flags below, which targets pageable memory and so waits for the stream
+    tr.mark("create: copies issued");
+    bool monotone = true;
+    std::vector<int> tiles = make_tiles(n, rs, &h->max_row, &monotone);
+    tr.mark("create: tiles cut (host)");
     CK(cudaMemcpyAsync(h->bad_host, bad, 2 * sizeof(int), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaFreeAsync(tmp, h->stream));
     CK(cudaFreeAsync(bad, h->stream));
-    // the row tiles are cut on the host while the copies are in flight
-    std::vector<int> tiles = make_tiles(n, rs, &h->max_row);
     CK(cudaStreamSynchronize(h->stream));
+    tr.mark("create: copies + checks done");
+    if (!monotone) return fail(MCR_DIMENSION, "rstart must be nondecreasing");
     if (h->bad_host[0]) return fail(MCR_DIMENSION, "column index out of range");
     if (h->bad_host[1]) return fail(MCR_DIMENSION, "rows must be sorted by column without duplicates");
-    return finish_create(h, n, rs, storage, &tiles);
+    const int rc = finish_create(h, n, rs, storage, &tiles);
+    tr.mark("create: finished");
+    return rc;
 }
 
 // A handle from a CSR already on the device (int64 row starts, int32 columns), copied.
@@ -333,13 +345,14 @@ int finish_create(mcr_matrix* h, int64_t n, const int64_t* rs, int storage,
     // off-diagonal row lengths
     {
         unsigned long long* fz = nullptr;
-        CK(cudaMallocAsync((void**)&fz, sizeof(unsigned long long), h->stream));
+        CK(cudaMallocAsync((void**)&fz, 2 * sizeof(unsigned long long), h->stream));
         CK(cudaMemsetAsync(fz, 0xff, sizeof(unsigned long long), h->stream));
+        CK(cudaMemsetAsync(fz + 1, 0, sizeof(unsigned long long), h->stream));
         CK(cudaMemsetAsync(h->offlen + n, 0, sizeof(long long), h->stream));
         k_diag<<<(int)std::min<int64_t>((n + 255) / 256, 1 << 16), 256, 0, h->stream>>>(
-            h->rp, h->col, h->val, (int)n, (long long)h->roff, h->d, h->offlen, fz);
+            h->rp, h->col, h->val, (int)n, (long long)h->roff, h->d, h->offlen, fz, fz + 1);
         CK(cudaGetLastError());
-        CK(cudaMemcpyAsync(&h->fz_host, fz, sizeof(h->fz_host), cudaMemcpyDeviceToHost,
+        CK(cudaMemcpyAsync(h->fz_host, fz, sizeof(h->fz_host), cudaMemcpyDeviceToHost,
                            h->stream));  // a handle field: outlives any early return
         CK(cudaFreeAsync(fz, h->stream));
     }
@@ -405,18 +418,23 @@ int finish_create(mcr_matrix* h, int64_t n, const int64_t* rs, int storage,
         if (stage) TRY(build_staged(h, storage == MCR_STORAGE_STAGED));
         CK(cudaStreamSynchronize(h->stream));
     }
-    h->first_zero = h->fz_host == ~0ull ? -1 : (long long)h->fz_host + h->roff;  // global row
+    h->first_zero = h->fz_host[0] == ~0ull ? -1 : (long long)h->fz_host[0] + h->roff;  // global row
+    h->nnz_off = nnz - (int64_t)h->fz_host[1];
     return MCR_OK;
 }
 
-int check_csr(int64_t n, const int64_t* rstart, const int64_t* col, const double* nonzero) {
+// `scan_rows` = false: the caller's upload path checks that rstart is nondecreasing itself
+// (make_tiles walks rstart anyway, while the copies are in flight).
+int check_csr(int64_t n, const int64_t* rstart, const int64_t* col, const double* nonzero,
+              bool scan_rows = true) {
     if (n < 0 || n >= INT_MAX) return fail(MCR_DIMENSION, "dimension out of range");
     if (n > 0 && (!rstart || (rstart[n] > 0 && (!col || !nonzero))))
         return fail(MCR_INVALID_ARGUMENT, "NULL CSR array");
     if (n > 0) {
-        if (rstart[0] != 0) return fail(MCR_DIMENSION, "malformed rstart vector");
-        for (int64_t i = 0; i < n; ++i)
-            if (rstart[i + 1] < rstart[i]) return fail(MCR_DIMENSION, "rstart must be nondecreasing");
+        if (rstart[0] != 0 || rstart[n] < 0) return fail(MCR_DIMENSION, "malformed rstart vector");
+        if (scan_rows)
+            for (int64_t i = 0; i < n; ++i)
+                if (rstart[i + 1] < rstart[i]) return fail(MCR_DIMENSION, "rstart must be nondecreasing");
     }
     return MCR_OK;
 }

@@ -18,10 +18,12 @@ __global__ void k_col64to32(const long long* __restrict__ in, int* __restrict__ 
 
 // Rows must be sorted by column without duplicates (the reference's CsrMatrix invariant,
 // sparse.py:101-118): the row sums are defined in that order.
+// Row bounds are clamped to [0, nnz]: rstart is checked for monotonicity on the host while
+// this runs, and a malformed one must not send the scan out of bounds.
 __global__ void k_check_rows(const long long* __restrict__ rp, const int* __restrict__ col, int n,
-                             int* bad) {
+                             long long nnz, int* bad) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-        for (long long e = rp[i] + 1; e < rp[i + 1]; ++e)
+        for (long long e = max(rp[i], 0ll) + 1, end = min(rp[i + 1], nnz); e < end; ++e)
             if (col[e] <= col[e - 1]) {
                 atomicExch(bad, 1);
                 break;
@@ -33,7 +35,8 @@ __global__ void k_check_rows(const long long* __restrict__ rp, const int* __rest
 // global row roff + i (row shards keep global column indices).
 __global__ void k_diag(const long long* __restrict__ rp, const int* __restrict__ col,
                        const double* __restrict__ val, int n, long long roff, double* d,
-                       long long* offlen, unsigned long long* first_zero) {
+                       long long* offlen, unsigned long long* first_zero,
+                       unsigned long long* ndiag) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         long long lo = rp[i], hi = rp[i + 1];
         const long long len = hi - lo;
@@ -49,6 +52,9 @@ __global__ void k_diag(const long long* __restrict__ rp, const int* __restrict__
         d[i] = dv;
         if (offlen) offlen[i] = len - has;
         if (dv == 0.0) atomicMin(first_zero, (unsigned long long)i);
+        const unsigned act = __activemask(), hb = __ballot_sync(act, has);  // one atomic per warp
+        if (ndiag && (threadIdx.x & 31) == __ffs(act) - 1 && hb)
+            atomicAdd(ndiag, (unsigned long long)__popc(hb));
     }
 }
 
