@@ -41,7 +41,8 @@ __global__ void __launch_bounds__(32) k_dense(const double* __restrict__ A, int 
             const int cols = min(DCOLS, npad - c * DCOLS);
             const uint32_t bytes = (uint32_t)(cols * DSLAB * sizeof(double));
             mbar_expect_tx(&bars[c], bytes);
-            bulk_g2s(dsm + c * DCOLS * DSLAB, src + (size_t)c * DCOLS * DSLAB, bytes, &bars[c]);
+            bulk_g2s_hint(dsm + c * DCOLS * DSLAB, src + (size_t)c * DCOLS * DSLAB, bytes, &bars[c],
+                          l2_evict_first());
         }
     }
     __syncwarp();
@@ -97,8 +98,8 @@ __global__ void __launch_bounds__(32) k_dense(const double* __restrict__ A, int 
             const int cc = min(DCOLS, npad - cn * DCOLS);
             const uint32_t bytes = (uint32_t)(cc * DSLAB * sizeof(double));
             mbar_expect_tx(&bars[stage], bytes);
-            bulk_g2s(dsm + stage * DCOLS * DSLAB, src + (size_t)cn * DCOLS * DSLAB, bytes,
-                     &bars[stage]);
+            bulk_g2s_hint(dsm + stage * DCOLS * DSLAB, src + (size_t)cn * DCOLS * DSLAB, bytes,
+                          &bars[stage], l2_evict_first());
         }
         xa = nxa;
         xb = nxb;

@@ -71,6 +71,7 @@ __global__ void __launch_bounds__(SP_THREADS, MCR_SP_MINB) k_spmv(Csr A, const d
     if (warp == SP_CONSUMERS / 32) {
         // ------------------------------------------------------------ producer warp
         if (lane == 0) {
+            const uint64_t pol = l2_evict_first();
             int t = blockIdx.x;
             TileDesc dn{};
             if (t < A.ntiles) dn = A.desc[t];
@@ -95,10 +96,10 @@ __global__ void __launch_bounds__(SP_THREADS, MCR_SP_MINB) k_spmv(Csr A, const d
                 const uint32_t vb = d.e1 > d.e0 ? (uint32_t)(((d.e1 - base) * 8 + 15) & ~15ll) : 0u;
                 const uint32_t cb = d.e1 > d.e0 ? (uint32_t)(((d.e1 - base) * 4 + 15) & ~15ll) : 0u;
                 mbar_expect_tx(&full_bar[s], rb + vb + cb);
-                bulk_g2s(stg[s].rp, A.rp + ra, rb, &full_bar[s]);
+                bulk_g2s_hint(stg[s].rp, A.rp + ra, rb, &full_bar[s], pol);
                 if (vb) {
-                    bulk_g2s(stg[s].val, A.val + base, vb, &full_bar[s]);
-                    bulk_g2s(stg[s].col, A.col + base, cb, &full_bar[s]);
+                    bulk_g2s_hint(stg[s].val, A.val + base, vb, &full_bar[s], pol);
+                    bulk_g2s_hint(stg[s].col, A.col + base, cb, &full_bar[s], pol);
                 }
             }
         }
