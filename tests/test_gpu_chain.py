@@ -126,3 +126,23 @@ def test_partition_states(gm, name):
     cls[sorted(part.prob_one)] = 1
     assert sha(cls) == c["classes_sha256"] and sha(part.uncertain) == c["uncertain_sha256"]
     assert all(part.index_of[int(s)] == i for i, s in enumerate(part.uncertain))
+
+
+@pytest.mark.parametrize("name", [n for n in NAMES if "jacobi-seq" in manifest()[n]
+                                  and "bicgstab-seq" in manifest()[n]])
+def test_reachability_on_staged_layout(gm, name, monkeypatch):
+    """The chain's M = I - A (negative off-diagonals) solved on the band-staged layout (AUTO
+    picks it for large systems; the cut is lowered to 0 here): the same bits as the tiles."""
+    from paper_1210_6412_b200.solvers import Breakdown, NotConverged
+    monkeypatch.setenv("MCR_STAGED_MIN_X_BYTES", "0")
+    c = manifest()[name]
+    ch, goals = chain(name)
+    for method, key in (("jacobi-gpu", "jacobi-seq"), ("bicgstab-gpu-exact", "bicgstab-seq")):
+        exp = c[key]
+        if exp["outcome"] != "ok":
+            with pytest.raises((NotConverged, Breakdown)):
+                gm.reachability_probabilities(ch, goals, method)
+            continue
+        x, rep = gm.reachability_probabilities(ch, goals, method)
+        assert rep.iterations == exp["iterations"]
+        assert sha(x) == exp["x_sha256"], (name, method)
