@@ -47,12 +47,10 @@ __global__ void __launch_bounds__(SP_THREADS, MCR_SP_MINB) k_spmv(Csr A, const d
     __shared__ double s_red[SP_THREADS / 32];
     __shared__ unsigned long long s_redu[SP_THREADS / 32];
     __shared__ int s_flag;
-    griddep_wait();
+    // The matrix does not depend on the previous kernel: the producer fills the first stages
+    // before waiting for it (with PDL this overlaps the previous kernel's tail); everything
+    // that reads vectors or the solver state waits first.
     griddep_launch();
-    if constexpr (epi_checks_stop<EPI>()) {
-        if (st->stop) return;
-    }
-    const double* xin = jacobi_select<EPI>(x, V, st);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
         for (int s = 0; s < SP_STAGES; ++s) {
@@ -75,12 +73,17 @@ __global__ void __launch_bounds__(SP_THREADS, MCR_SP_MINB) k_spmv(Csr A, const d
             int t = blockIdx.x;
             TileDesc dn{};
             if (t < A.ntiles) dn = A.desc[t];
+            bool stopped = false;
             for (int i = 0;; ++i, t += G) {
                 const int s = i % SP_STAGES;
                 const TileDesc d = dn;
                 if (t + G < A.ntiles) dn = A.desc[t + G];  // prefetch the next descriptor
+                if (i == SP_STAGES) {  // first stages issued: now the stop flag is needed
+                    griddep_wait();
+                    if constexpr (epi_checks_stop<EPI>()) stopped = ld_state(&st->stop) != 0;
+                }
                 if (i >= SP_STAGES) mbar_wait(&empty_bar[s], (uint32_t)(((i / SP_STAGES) + 1) & 1));
-                if (t >= A.ntiles) {
+                if (t >= A.ntiles || stopped) {
                     s_tile[s] = -1;
                     mbar_arrive(&full_bar[s]);
                     break;
@@ -106,11 +109,20 @@ __global__ void __launch_bounds__(SP_THREADS, MCR_SP_MINB) k_spmv(Csr A, const d
         __syncwarp();
     } else {
         // ------------------------------------------------------------ consumer warps
+        griddep_wait();
+        bool stopped = false;
+        if constexpr (epi_checks_stop<EPI>()) stopped = ld_state(&st->stop) != 0;
+        const double* xin = jacobi_select<EPI>(x, V, st);
         for (int i = 0;; ++i) {
             const int s = i % SP_STAGES;
             mbar_wait(&full_bar[s], (uint32_t)((i / SP_STAGES) & 1));
             const int t = s_tile[s];
             if (t < 0) break;
+            if (stopped) {  // the solve has stopped: only release the prefetched stages
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty_bar[s]);
+                continue;
+            }
             const TileDesc d = s_desc[s];
             const int nrows = d.r1 - d.r0;
             const int row = d.r0 + tid;
@@ -188,6 +200,10 @@ __global__ void __launch_bounds__(SP_THREADS, MCR_SP_MINB) k_spmv(Csr A, const d
                 if (tid == 0) V.P2[blockIdx.x] = acc2;
             }
         }
+    }
+    griddep_wait();  // (the producer lane may have ended before its wait)
+    if constexpr (epi_checks_stop<EPI>()) {
+        if (ld_state(&st->stop)) return;  // stopped before this kernel: no partials, no step
     }
     if constexpr (EPI == EPI_JACOBI) {
         if (V.peers) __threadfence_system();  // peer stores performed before the grid retires
