@@ -189,6 +189,7 @@ struct mcr_matrix {
     int seqdots = 0;
     int spmv_grid = 1;
     int small_grid = 0;                     // > 0: whole solve in one cooperative launch
+    bool small_cluster = false;             // ... launched as one thread-block cluster
     unsigned long long* maxslot = nullptr;  // 3 slots for the persistent solvers
     std::mutex mu;
 

@@ -13,6 +13,7 @@ namespace mcr {
 // round trip through global state.
 namespace cg = cooperative_groups;
 constexpr int SM_NT = TILE_ROWS;
+constexpr int SMALL_CLUSTER_MAX = 16;  // CTAs of the cluster variant (non-portable above 8)
 
 struct SmallSmem {
     double val[TILE_NNZ];      // this CTA's tile, loaded once per solve
@@ -21,8 +22,54 @@ struct SmallSmem {
     int rp[TILE_ROWS + 1];
     double red[SM_NT / 32];
     unsigned long long redu[SM_NT / 32];
+    double part[4];                 // cluster variant: this CTA's dot partials (q.v, t.t, t.s, q.r)
+    unsigned long long mx[3];       // cluster variant: this CTA's max|.| bits per slot
     long long e0, e1;
     int nrows, r0, cached;
+};
+
+// ---------------------------------------------------------------- barrier / exchange policy
+// CL = false: one cooperative grid, grid.sync() between phases, partials and maxima through
+// global memory. CL = true: the whole grid is ONE thread-block cluster (<= 16 CTAs, one per SM):
+// the hardware cluster barrier replaces the grid barrier and every CTA reads the others'
+// partials and maxima straight from their shared memory (DSMEM), which removes the global
+// round trips that dominate an iteration of these latency-bound systems. Vectors written by
+// other CTAs are then gathered through L2 (ld.global.cg): a cluster barrier orders memory but
+// does not clean this SM's L1.
+__device__ __forceinline__ void cluster_barrier() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+template <class T>
+__device__ __forceinline__ T dsmem_load(const T* p, int rank);
+template <>
+__device__ __forceinline__ double dsmem_load<double>(const double* p, int rank) {
+    uint32_t ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(p)), "r"(rank));
+    double v;
+    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(ra) : "memory");
+    return v;
+}
+template <>
+__device__ __forceinline__ unsigned long long dsmem_load<unsigned long long>(const unsigned long long* p,
+                                                                             int rank) {
+    uint32_t ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(p)), "r"(rank));
+    unsigned long long v;
+    asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(ra) : "memory");
+    return v;
+}
+
+template <bool CL>
+struct SmallSync {
+    __device__ __forceinline__ void sync() {
+        if constexpr (CL) cluster_barrier();
+        else cg::this_grid().sync();
+    }
+    template <class T>
+    __device__ __forceinline__ T gather(const T* p) const {
+        if constexpr (CL) return __ldcg(p);
+        else return *p;
+    }
 };
 
 // One tile per CTA (grid == ntiles): its row pointers, columns and values move to shared
@@ -99,13 +146,32 @@ __device__ __forceinline__ double read_max(unsigned long long* slot) {
     return bits2d(__ldcg(slot));
 }
 
-// Jacobi, all sweeps in one launch. maxslot[3] are zero on entry. Each thread keeps its row's
-// b, d and current iterate in registers; per sweep only the gathers, the x' store and one
-// grid barrier remain.
+// all_reduce_partials over the CTAs' shared-memory slots of one cluster: the same operations
+// in the same order (0.0 + P[k] per thread, then the CTA tree), so the same bits.
+__device__ __forceinline__ double cluster_reduce_partials(const double* slot, int count, double* red) {
+    double acc = 0.0;
+    for (int k = threadIdx.x; k < count; k += SM_NT) acc = dadd(acc, dsmem_load(slot, k));
+    acc = group_sum<SM_NT / 32, 0>(acc, red);
+    if (threadIdx.x == 0) red[0] = acc;
+    __syncthreads();
+    acc = red[0];
+    __syncthreads();
+    return acc;
+}
+__device__ __forceinline__ double cluster_read_max(const unsigned long long* slot, int count) {
+    unsigned long long m = 0;
+    for (int k = 0; k < count; ++k) m = umax(m, dsmem_load(slot, k));
+    return bits2d(m);
+}
+
+// Jacobi, all sweeps in one launch. maxslot[3] are zero on entry (grid variant). Each thread
+// keeps its row's b, d and current iterate in registers; per sweep only the gathers, the x'
+// store and one barrier remain.
+template <bool CL>
 __global__ void __launch_bounds__(SM_NT) k_jacobi_small(Csr R, Vecs V, SolveState* st,
                                                         unsigned long long* maxslot) {
     __shared__ SmallSmem sm;
-    cg::grid_group grid = cg::this_grid();
+    SmallSync<CL> bar;
     const double tol = st->tol;
     const long long max_it = st->max_it;
     load_tile(R, blockIdx.x, sm);
@@ -118,7 +184,7 @@ __global__ void __launch_bounds__(SM_NT) k_jacobi_small(Csr R, Vecs V, SolveStat
         ++it;
         const double* xin = (it & 1) ? V.x_jac0 : V.x_jac1;
         double* xout = (it & 1) ? V.x_jac1 : V.x_jac0;
-        const double s = tile_rowsum(R, sm, [&](int c) { return xin[c]; });
+        const double s = tile_rowsum(R, sm, [&](int c) { return bar.gather(xin + c); });
         unsigned long long mb = 0;
         if (row >= 0) {
             const double xn = ddiv(dsub(bi, s), di);   // (b - R x) / d
@@ -127,12 +193,21 @@ __global__ void __launch_bounds__(SM_NT) k_jacobi_small(Csr R, Vecs V, SolveStat
             xi = xn;
         }
         mb = group_max<SM_NT / 32, 0>(mb, sm.redu);
-        if (threadIdx.x == 0 && mb) atomicMax(&maxslot[it % 3], mb);
-        // slot (it+1)%3 was last read before the previous barrier by every CTA: clear it for
-        // the next sweep before this barrier, so no CTA can add to it before it is cleared
-        if (blockIdx.x == 0 && threadIdx.x == 0) maxslot[(it + 1) % 3] = 0ull;
-        grid.sync();
-        const double md = read_max(&maxslot[it % 3]);
+        double md;
+        if constexpr (CL) {
+            // slot it&1 is rewritten two sweeps later, after every CTA has passed the barrier
+            // that follows its reads
+            if (threadIdx.x == 0) sm.mx[it & 1] = mb;
+            bar.sync();
+            md = cluster_read_max(&sm.mx[it & 1], (int)gridDim.x);
+        } else {
+            if (threadIdx.x == 0 && mb) atomicMax(&maxslot[it % 3], mb);
+            // slot (it+1)%3 was last read before the previous barrier by every CTA: clear it for
+            // the next sweep before this barrier, so no CTA can add to it before it is cleared
+            if (blockIdx.x == 0 && threadIdx.x == 0) maxslot[(it + 1) % 3] = 0ull;
+            bar.sync();
+            md = read_max(&maxslot[it % 3]);
+        }
         if (md <= tol) stop = CONVERGED;
         else if (it >= max_it) stop = NOTCONV;
     }
@@ -140,6 +215,7 @@ __global__ void __launch_bounds__(SM_NT) k_jacobi_small(Csr R, Vecs V, SolveStat
         st->it = it;
         st->stop = stop;
     }
+    if constexpr (CL) cluster_barrier();  // no CTA leaves while others may read its slots
 }
 
 // BiCGStab, whole solve in one launch (solvers.py:450-491), three grid barriers per iteration.
@@ -152,11 +228,12 @@ __global__ void __launch_bounds__(SM_NT) k_jacobi_small(Csr R, Vecs V, SolveStat
 // still read the previous pair while this iteration's is written. Partials live in four
 // separate slots (parts + k*pstride: q.v, t.t, t.s, q.r) because no barrier separates a
 // slot's all-reduce from the next slot's writes. maxslot[2] zero on entry.
+template <bool CL>
 __global__ void __launch_bounds__(SM_NT) k_bicg_small(Csr A, Vecs V, SolveState* st,
                                                       unsigned long long* maxslot, double* parts,
                                                       int pstride) {
     __shared__ SmallSmem sm;
-    cg::grid_group grid = cg::this_grid();
+    SmallSync<CL> bar;
     const double tol = st->tol;
     const long long max_it = st->max_it;
     const int nt = A.ntiles;
@@ -164,6 +241,29 @@ __global__ void __launch_bounds__(SM_NT) k_bicg_small(Csr A, Vecs V, SolveState*
     double* Ptt = parts + pstride;
     double* Pts = parts + 2 * pstride;
     double* Pqr = parts + 3 * pstride;
+    enum { S_QV = 0, S_TT = 1, S_TS = 2, S_QR = 3 };
+    // publish this CTA's partial of slot k (thread 0 holds it), then (after a barrier) the
+    // fixed-order all-reduce over the CTAs
+    auto publish = [&](int k, double* gslot, double v) {
+        if (threadIdx.x == 0) {
+            if constexpr (CL) sm.part[k] = v;
+            else gslot[blockIdx.x] = v;
+        }
+    };
+    auto allreduce = [&](int k, const double* gslot) {
+        if constexpr (CL) return cluster_reduce_partials(&sm.part[k], nt, sm.red);
+        else return all_reduce_partials(gslot, nt, sm.red);
+    };
+    auto publish_max = [&](int k, unsigned long long m) {  // m valid in thread 0
+        if (threadIdx.x == 0) {
+            if constexpr (CL) sm.mx[k] = m;
+            else if (m) atomicMax(&maxslot[k], m);
+        }
+    };
+    auto read_maxk = [&](int k) {
+        if constexpr (CL) return cluster_read_max(&sm.mx[k], nt);
+        else return read_max(&maxslot[k]);
+    };
     double* Rg = V.r;
     load_tile(A, blockIdx.x, sm);
     const int tid = threadIdx.x;
@@ -172,7 +272,7 @@ __global__ void __launch_bounds__(SM_NT) k_bicg_small(Csr A, Vecs V, SolveState*
     if (row >= 0) { xi = V.x[row]; bi = V.b[row]; }
     // setup: r = b - 1.0 * M x0, q = r, p = v = 0
     const double* X = V.x;
-    const double s0 = tile_rowsum(A, sm, [&](int c) { return X[c]; });
+    const double s0 = tile_rowsum(A, sm, [&](int c) { return bar.gather(X + c); });
     double ri = 0.0, qi = 0.0, pi = 0.0, vi = 0.0;
     unsigned long long mb = 0;
     double p1 = 0.0;
@@ -186,16 +286,16 @@ __global__ void __launch_bounds__(SM_NT) k_bicg_small(Csr A, Vecs V, SolveState*
         p1 = dmul(ri, ri);
     }
     p1 = group_sum<SM_NT / 32, 0>(p1, sm.red);
-    if (tid == 0) Pqr[blockIdx.x] = p1;
+    publish(S_QR, Pqr, p1);
     mb = group_max<SM_NT / 32, 0>(mb, sm.redu);
-    if (tid == 0 && mb) atomicMax(&maxslot[0], mb);
-    grid.sync();
+    publish_max(0, mb);
+    bar.sync();
     int stop = RUNNING, which = 0;
     long long it = 0, bd_it = 0;
     double y = 1.0, a = 1.0, w = 1.0, beta = 0.0;
     {
-        const double mr = read_max(&maxslot[0]);
-        const double qr = all_reduce_partials(Pqr, nt, sm.red);
+        const double mr = read_maxk(0);
+        const double qr = allreduce(S_QR, Pqr);
         if (mr <= tol) {
             stop = CONVERGED;
         } else {
@@ -214,7 +314,7 @@ __global__ void __launch_bounds__(SM_NT) k_bicg_small(Csr A, Vecs V, SolveState*
         double* Vnew = odd ? V.t : V.v;
         // v = M p with p = r + beta (p - w v) formed at each gathered column
         const double sv = tile_rowsum(A, sm, [&](int c) {
-            return dadd(Rg[c], dmul(beta, dsub(Pold[c], dmul(w, Vold[c]))));
+            return dadd(bar.gather(Rg + c), dmul(beta, dsub(bar.gather(Pold + c), dmul(w, bar.gather(Vold + c)))));
         });
         p1 = 0.0;
         if (row >= 0) {
@@ -225,15 +325,17 @@ __global__ void __launch_bounds__(SM_NT) k_bicg_small(Csr A, Vecs V, SolveState*
             p1 = dmul(qi, vi);
         }
         p1 = group_sum<SM_NT / 32, 0>(p1, sm.red);
-        if (tid == 0) Pqv[blockIdx.x] = p1;
-        if (blockIdx.x == 0 && tid == 0) maxslot[1] = 0ull;
-        grid.sync();
-        const double qv = all_reduce_partials(Pqv, nt, sm.red);
+        publish(S_QV, Pqv, p1);
+        if constexpr (!CL) {
+            if (blockIdx.x == 0 && tid == 0) maxslot[1] = 0ull;
+        }
+        bar.sync();
+        const double qv = allreduce(S_QV, Pqv);
         if (tiny(qv)) { stop = BREAKDOWN; which = 2; bd_it = cur; break; }
         a = ddiv(y, qv);
         // t = M s with s = r - a v formed at each gathered column; s, max|s| for own rows
         const double st_ = tile_rowsum(A, sm, [&](int c) {
-            return dsub(Rg[c], dmul(a, Vnew[c]));
+            return dsub(bar.gather(Rg + c), dmul(a, bar.gather(Vnew + c)));
         });
         double si = 0.0, ti = 0.0, p2 = 0.0;
         p1 = 0.0;
@@ -246,14 +348,15 @@ __global__ void __launch_bounds__(SM_NT) k_bicg_small(Csr A, Vecs V, SolveState*
             p2 = dmul(ti, si);
         }
         mb = group_max<SM_NT / 32, 0>(mb, sm.redu);
-        if (tid == 0 && mb) atomicMax(&maxslot[1], mb);
+        publish_max(1, mb);
         p1 = group_sum<SM_NT / 32, 0>(p1, sm.red);
         p2 = group_sum<SM_NT / 32, 0>(p2, sm.red);
-        if (tid == 0) { Ptt[blockIdx.x] = p1; Pts[blockIdx.x] = p2; }
-        grid.sync();
-        const bool small = read_max(&maxslot[1]) <= tol;
-        const double tt = all_reduce_partials(Ptt, nt, sm.red);
-        const double ts = all_reduce_partials(Pts, nt, sm.red);
+        publish(S_TT, Ptt, p1);
+        publish(S_TS, Pts, p2);
+        bar.sync();
+        const bool small = read_maxk(1) <= tol;
+        const double tt = allreduce(S_TT, Ptt);
+        const double ts = allreduce(S_TS, Pts);
         if (tiny(tt)) {
             if (!small) { stop = BREAKDOWN; which = 3; bd_it = cur; break; }
             w = 0.0;
@@ -269,12 +372,12 @@ __global__ void __launch_bounds__(SM_NT) k_bicg_small(Csr A, Vecs V, SolveState*
             p1 = dmul(qi, ri);
         }
         p1 = group_sum<SM_NT / 32, 0>(p1, sm.red);
-        if (tid == 0) Pqr[blockIdx.x] = p1;
-        grid.sync();
+        publish(S_QR, Pqr, p1);
+        bar.sync();
         it = cur;
         if (small) { stop = CONVERGED; break; }
         if (it >= max_it) { stop = NOTCONV; break; }
-        const double qr = all_reduce_partials(Pqr, nt, sm.red);
+        const double qr = allreduce(S_QR, Pqr);
         const double denom = dmul(y, w);
         y = qr;
         if (tiny(denom)) { stop = BREAKDOWN; which = 1; bd_it = it + 1; break; }
@@ -287,6 +390,7 @@ __global__ void __launch_bounds__(SM_NT) k_bicg_small(Csr A, Vecs V, SolveState*
         st->which = which;
         st->bd_it = bd_it;
     }
+    if constexpr (CL) cluster_barrier();  // no CTA leaves while others may read its slots
 }
 
 }  // namespace mcr

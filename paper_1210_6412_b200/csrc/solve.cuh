@@ -21,6 +21,30 @@ int read_state(mcr_matrix* h) {
 }
 
 // ---------------------------------------------------------------- kernel launchers
+// Whole-solve small kernels: one cluster (CL) or one cooperative grid.
+template <typename... KArgs, typename... Args>
+int launch_small(mcr_matrix* h, void (*cluster_kern)(KArgs...), void (*grid_kern)(KArgs...),
+                 Args... args) {
+    if (h->small_cluster) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(h->small_grid);
+        cfg.blockDim = dim3(SM_NT);
+        cfg.stream = h->stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = h->small_grid;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        CK(cudaLaunchKernelEx(&cfg, cluster_kern, static_cast<KArgs>(args)...));
+    } else {
+        void* a[] = {(void*)&args...};
+        CK(cudaLaunchCooperativeKernel((void*)grid_kern, h->small_grid, SM_NT, a, 0, h->stream));
+    }
+    return MCR_OK;
+}
+
 // Every solve kernel goes out with programmatic stream serialization (PDL): the next kernel
 // of the chain is scheduled while the current one drains, and waits in griddepcontrol.wait.
 template <typename... KArgs, typename... Args>
@@ -187,9 +211,8 @@ int jacobi_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double tol
     int batch = 4;
     if (h->small_grid > 0) {
         CK(cudaMemsetAsync(h->maxslot, 0, 3 * sizeof(unsigned long long), h->stream));
-        Csr R = csr_off(h);
-        void* args[] = {&R, &V, &h->st, &h->maxslot};
-        CK(cudaLaunchCooperativeKernel((void*)k_jacobi_small, h->small_grid, SM_NT, args, 0, h->stream));
+        TRY(launch_small(h, k_jacobi_small<true>, k_jacobi_small<false>, csr_off(h), V, h->st,
+                         h->maxslot));
         ++launched;
         TRY(read_state(h));
     } else for (;;) {
@@ -243,11 +266,9 @@ int bicgstab_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double t
     int batch = 4;
     if (h->small_grid > 0 && !h->seqdots) {
         CK(cudaMemsetAsync(h->maxslot, 0, 3 * sizeof(unsigned long long), h->stream));
-        Csr A = csr_full(h);
-        double* parts = h->P;
-        int pstride = h->nunits;  // four partial slots of nunits >= ntiles doubles each
-        void* args[] = {&A, &V, &h->st, &h->maxslot, &parts, &pstride};
-        CK(cudaLaunchCooperativeKernel((void*)k_bicg_small, h->small_grid, SM_NT, args, 0, h->stream));
+        // four partial slots of nunits >= ntiles doubles each (grid variant)
+        TRY(launch_small(h, k_bicg_small<true>, k_bicg_small<false>, csr_full(h), V, h->st,
+                         h->maxslot, h->P, h->nunits));
         ++launched;
         TRY(read_state(h));
         iters = max_it;  // the loop below has nothing left to do

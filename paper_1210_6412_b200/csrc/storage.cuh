@@ -188,6 +188,40 @@ static int set_kernel_attributes() {
 int finish_create(mcr_matrix* h, int64_t n, const int64_t* rs, int storage,
                          std::vector<int>* pre_tiles = nullptr);
 
+// Can a cluster of `ctas` small-solver CTAs be scheduled (<= 8 portable, 16 non-portable)?
+bool small_cluster_ok(int ctas) {
+    static int ok16 = -1;
+    if (ok16 < 0) {
+        ok16 = cudaFuncSetAttribute(k_jacobi_small<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+                       cudaSuccess &&
+                   cudaFuncSetAttribute(k_bicg_small<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+                       cudaSuccess;
+        cudaGetLastError();
+    }
+    if (ctas > 8 && !ok16) return false;
+    for (int which = 0; which < 2; ++which) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(ctas);
+        cfg.blockDim = dim3(SM_NT);
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = ctas;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int clusters = 0;
+        const cudaError_t e = which == 0
+                                  ? cudaOccupancyMaxActiveClusters(&clusters, k_jacobi_small<true>, &cfg)
+                                  : cudaOccupancyMaxActiveClusters(&clusters, k_bicg_small<true>, &cfg);
+        if (e != cudaSuccess || clusters < 1) {
+            cudaGetLastError();
+            return false;
+        }
+    }
+    return true;
+}
+
 int init_handle(mcr_matrix* h) {
     TRY(keep_pool_memory(h->device));
     CK(cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking));
@@ -397,13 +431,16 @@ int finish_create(mcr_matrix* h, int64_t n, const int64_t* rs, int storage,
                             (storage == MCR_STORAGE_AUTO &&
                              8.0 * (double)h->n_full() >= auto_bytes));
         int pj = 0, pb = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pj, k_jacobi_small, SM_NT, 0));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pb, k_bicg_small, SM_NT, 0));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pj, k_jacobi_small<false>, SM_NT, 0));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pb, k_bicg_small<false>, SM_NT, 0));
         const int coresident = sms * std::min(pj, pb);
         // one tile per CTA keeps the per-sweep critical path to a single tile
         if (!h->use_sell && !h->sharded() && !stage && storage != MCR_STORAGE_TILES_STREAM &&
             h->ntiles <= coresident && h->ntiles <= 2 * sms)
             h->small_grid = h->ntiles;
+        // up to 16 tiles: the whole grid as one thread-block cluster (cluster barriers, DSMEM)
+        if (h->small_grid > 0 && h->small_grid <= SMALL_CLUSTER_MAX && !std::getenv("MCR_NO_CLUSTER"))
+            h->small_cluster = small_cluster_ok(h->small_grid);
         TRY(dalloc(h, &h->maxslot, 3));
         TRY(dalloc(h, &h->tile_row, tiles.size()));
         CK(cudaMemcpyAsync(h->tile_row, tiles.data(), sizeof(int) * tiles.size(),
