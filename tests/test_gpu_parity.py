@@ -347,3 +347,26 @@ def test_plugin_registers_into_reference():
     assert np.array_equal(got.x, ref.x) and got.iterations == ref.iterations
     with pytest.raises(NotConverged):
         reg["bicgstab-gpu"](m, b, SolverConfig(max_iterations=1))
+
+
+@pytest.mark.parametrize("name", ["kat_golden2x2", "c4_2000_3999", "grid_50_5", "kat_breakdown_qv",
+                                  "seeded_guess", "kat_divergent"])
+def test_small_cluster_equals_grid(gs, name, monkeypatch):
+    """Systems of <= 16 tiles run the whole-solve kernels as one thread-block cluster; the
+    cooperative-grid variant (MCR_NO_CLUSTER) must give the same bits, outcome and count."""
+    from paper_1210_6412_b200 import _lib
+    m, b = system(name)
+    out = []
+    for env in (None, "1"):
+        if env:
+            monkeypatch.setenv("MCR_NO_CLUSTER", env)
+        dm = gs.DeviceMatrix(m, 0, 0)
+        try:
+            res = []
+            for method in ("jacobi", "bicgstab"):
+                rc, x, rep = dm.solve(method, b, None, 1e-10, 500)
+                res.append((rc, int(rep.iterations), x.tobytes(), float(rep.residual_inf).hex()))
+            out.append(res)
+        finally:
+            dm.close()
+    assert out[0] == out[1]
