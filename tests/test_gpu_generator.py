@@ -114,3 +114,49 @@ def test_sharded_generated_solve_bit_identical(mods):
     assert all(r is not None for r in reps)
     assert all(r.iterations == rep1.iterations for r in reps)
     assert np.array_equal(np.concatenate(xs), x1)
+
+
+def test_large_generated_staged_equals_tiles(mods):
+    """Beyond L2 (n = 2e7, x = 160 MB) AUTO picks the band-staged layout; at full size its SpMV
+    and Jacobi iterates are bit-identical to the tiled CSR kernels (a size-independent check:
+    the oracle would take minutes here), and the BiCGStab solution agrees within 1e-9."""
+    import ctypes
+    import torch
+    from paper_1210_6412_b200 import _lib
+    dist, gs = mods
+    n, seed = 20_000_000, 9
+    L = _lib.load()
+    staged = gs.DeviceMatrix.generated(n, 7.0, 1, 10, seed)
+    tiles = gs.DeviceMatrix.generated(n, 7.0, 1, 10, seed, storage=_lib.STORAGE_TILES_STREAM)
+    try:
+        assert staged.info()["storage"] == _lib.STORAGE_STAGED
+        assert tiles.info()["storage"] == _lib.STORAGE_TILES
+        dev = torch.device("cuda", 0)
+        x = torch.rand(n, dtype=torch.float64, device=dev, generator=torch.Generator(dev).manual_seed(3))
+        ys = torch.empty_like(x)
+        yt = torch.empty_like(x)
+        for dm, y in ((staged, ys), (tiles, yt)):
+            assert L.mcr_matvec_device(dm.handle, ctypes.c_void_p(x.data_ptr()),
+                                       ctypes.c_void_p(y.data_ptr())) == _lib.MCR_OK
+        torch.cuda.synchronize()
+        assert torch.equal(ys, yt)
+        b = torch.empty(n, dtype=torch.float64, device=dev)
+        staged.generated_rhs(seed, b.data_ptr())
+        out = []
+        for dm in (staged, tiles):
+            res = []
+            for fn, it in ((L.mcr_jacobi_device, 25), (L.mcr_bicgstab_device, 10_000)):
+                xo = torch.empty(n, dtype=torch.float64, device=dev)
+                rep = _lib.Report()
+                rc = fn(dm.handle, ctypes.c_void_p(b.data_ptr()), None, 1e-10, it,
+                        ctypes.c_void_p(xo.data_ptr()), ctypes.byref(rep))
+                assert rc in (_lib.MCR_OK, _lib.MCR_NOT_CONVERGED), _lib.last_error()
+                res.append((rep.iterations, float(rep.residual_inf), xo))
+            out.append(res)
+        (js, bs), (jt, bt) = out
+        assert js[0] == jt[0] and js[1] == jt[1] and torch.equal(js[2], jt[2])  # Jacobi: exact
+        assert abs(bs[0] - bt[0]) <= 2                                           # BiCGStab: dots
+        assert float((bs[2] - bt[2]).abs().max()) / max(1.0, float(bt[2].abs().max())) <= 1e-9
+    finally:
+        staged.close()
+        tiles.close()
