@@ -62,7 +62,6 @@ struct SolveState {
     double tol;
     unsigned long long maxbits;  // atomicMax of |.| bit patterns (non-negative doubles order as u64)
     unsigned int done;           // last-CTA counter
-    unsigned int tile_ctr;       // dynamic tile scheduler of k_spmv
     unsigned long long p1_ctr;   // chunk tickets of the staged products pass (staged.cuh)
     double y, a, w, beta, qv, tt, ts, resid;
     int small;
@@ -150,13 +149,7 @@ __device__ __forceinline__ unsigned long long umax(unsigned long long a, unsigne
     return a > b ? a : b;
 }
 __device__ __forceinline__ bool tiny(double v) { return v == 0.0 || fabs(v) < TINY; }
-// Ordered loads (asm volatile keeps their issue order): streaming vector loads first, then the
-// solver state, so the state's L2 round trip overlaps the stream instead of gating it.
-__device__ __forceinline__ double ld_stream(const double* p) {
-    double v;
-    asm volatile("ld.global.cs.f64 %0, [%1];" : "=d"(v) : "l"(p));
-    return v;
-}
+// Solver-state loads through L2 (asm volatile keeps their place in the issue order).
 __device__ __forceinline__ double ld_state(const double* p) {
     double v;
     asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p));
@@ -448,13 +441,12 @@ __device__ __forceinline__ void kernel_finish(const Vecs& V, SolveState* st, int
             st->send[2] = bits2d(atomicExch(&st->maxbits, 0ull));
             st->send[3] = 0.0;
             st->done = 0;
-            st->tile_ctr = 0;
         }
         return;
     }
     if constexpr (epi_has_dot<EPI>()) {
         if (st->seqdots) {  // k_seqdot runs the reference-order dots and finalises
-            if (threadIdx.x == 0) { st->done = 0; st->tile_ctr = 0; }
+            if (threadIdx.x == 0) st->done = 0;
             return;
         }
     }
@@ -463,7 +455,6 @@ __device__ __forceinline__ void kernel_finish(const Vecs& V, SolveState* st, int
     if constexpr (EPI == EPI_T) r2 = reduce_partials<NT>(V.P2, nunits, s_red);
     if (threadIdx.x != 0) return;
     st->done = 0;
-    st->tile_ctr = 0;
     if constexpr (EPI == EPI_RESID) {
         st->resid = bits2d(atomicExch(&st->maxbits, 0ull));
     } else if constexpr (EPI == EPI_JACOBI) {
