@@ -64,6 +64,8 @@ struct SolveState {
     unsigned int done;           // last-CTA counter
     unsigned long long p1_ctr;   // chunk tickets of the staged products pass (staged.cuh)
     double y, a, w, beta, qv, tt, ts, resid;
+    double last;         // convergence measure of the latest sweep / iteration (Jacobi max|x'-x|,
+                         // BiCGStab max|s|): the host sizes its batches from its decay
     int small;
     int seqdots;  // 1: inner products by k_seqdot (reference order, bit-exact), not the tree
     int sharded;  // 1: row shard of a multi-GPU system -- reduction kernels publish their local
@@ -345,6 +347,7 @@ __device__ __forceinline__ void fin_v(SolveState* st, double qv) {
 }
 __device__ __forceinline__ void fin_t(SolveState* st, double tt, double ts) {
     const double ms = bits2d(atomicExch(&st->maxbits, 0ull));
+    st->last = ms;
     const int small = ms <= st->tol;                // solvers.py:476
     st->small = small;
     st->tt = tt;
@@ -461,6 +464,7 @@ __device__ __forceinline__ void kernel_finish(const Vecs& V, SolveState* st, int
         const double md = bits2d(atomicExch(&st->maxbits, 0ull));
         const long long it = st->it + 1;
         st->it = it;
+        st->last = md;
         if (md <= st->tol) st->stop = CONVERGED;       // NaN compares false: keep going
         else if (it >= st->max_it) st->stop = NOTCONV;
     } else if constexpr (EPI == EPI_S0) {

@@ -191,6 +191,7 @@ __global__ void k_finalize(SolveState* st, const double* __restrict__ recv, int 
         const double md = bits2d(mb);
         const long long it = st->it + 1;
         st->it = it;
+        st->last = md;
         if (md <= st->tol) st->stop = CONVERGED;
         else if (it >= st->max_it) st->stop = NOTCONV;
     } else if constexpr (W == FIN_RESID) {
