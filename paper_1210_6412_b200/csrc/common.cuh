@@ -64,6 +64,8 @@ struct SolveState {
     unsigned int done;           // last-CTA counter
     unsigned long long p1_ctr;   // chunk tickets of the staged products pass (staged.cuh)
     double y, a, w, beta, qv, tt, ts, resid;
+    unsigned long long cond;  // graph mode: the while-node's conditional handle (0 = none);
+                              // the kernel that decides the stop clears it
     double last;         // convergence measure of the latest sweep / iteration (Jacobi max|x'-x|,
                          // BiCGStab max|s|): the host sizes its batches from its decay
     int small;
@@ -308,6 +310,12 @@ __device__ __forceinline__ bool last_cta(unsigned int* ctr, int* s_flag) {
     const bool last = *s_flag != 0;
     if (last) __threadfence();
     return last;
+}
+
+// Graph mode (solve.cuh): the solve loop is a CUDA-graph while node; the kernel that takes
+// the stop decision keeps it running (1) or ends it (0). Thread 0 of the deciding CTA.
+__device__ __forceinline__ void graph_continue(SolveState* st) {
+    if (st->cond) cudaGraphSetConditional((cudaGraphConditionalHandle)st->cond, st->stop == RUNNING ? 1u : 0u);
 }
 
 // ---------------------------------------------------------------- BiCGStab scalar steps

@@ -187,6 +187,15 @@ struct mcr_matrix {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int64_t bytes = 0;
     int seqdots = 0;
+    // graph mode (solve.cuh): the whole iteration loop as one CUDA graph with a while node
+    struct GraphLoop {
+        cudaGraphExec_t exec = nullptr;
+        cudaGraph_t graph = nullptr;
+        unsigned long long cond = 0;
+        int unroll = 1;
+        bool failed = false;
+    } gl_bicg;
+    int bicg_solves = 0;
     int spmv_grid = 1;
     int small_grid = 0;                     // > 0: whole solve in one cooperative launch
     bool small_cluster = false;             // ... launched as one thread-block cluster

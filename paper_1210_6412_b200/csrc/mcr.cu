@@ -50,6 +50,10 @@ MCR_API void mcr_matrix_destroy(mcr_matrix* h) {
                 if (p) cudaFreeAsync(p, s);
             cudaStreamSynchronize(s);
         }
+        for (auto* gl : {&h->gl_bicg}) {
+            if (gl->exec) cudaGraphExecDestroy(gl->exec);
+            if (gl->graph) cudaGraphDestroy(gl->graph);
+        }
         for (void* p : h->ipc_opened) cudaIpcCloseMemHandle(p);
         if (h->fullblk) cudaFree(h->fullblk);
         if (h->d_peers) cudaFree(h->d_peers);

@@ -91,7 +91,10 @@ __global__ void __launch_bounds__(CHUNK_NT) k_phase(Vecs V, int n, SolveState* s
         if (threadIdx.x == 0) V.P1[blockIdx.x] = part;
         if (!last_cta(&st->done, &s_flag)) return;
         if (st->seqdots || stop) {
-            if (threadIdx.x == 0) st->done = 0;
+            if (threadIdx.x == 0) {
+                st->done = 0;
+                if (stop) graph_continue(st);  // stopped earlier in this iteration
+            }
             return;
         }
         const double qr = reduce_partials<CHUNK_NT>(V.P1, gridDim.x, s_red);
@@ -105,6 +108,7 @@ __global__ void __launch_bounds__(CHUNK_NT) k_phase(Vecs V, int n, SolveState* s
             return;
         }
         fin_e(st, qr);
+        graph_continue(st);
     }
 }
 

@@ -370,3 +370,32 @@ def test_small_cluster_equals_grid(gs, name, monkeypatch):
         finally:
             dm.close()
     assert out[0] == out[1]
+
+
+@pytest.mark.parametrize("name", ["c2_trial0", "c1_seed77", "kat_breakdown_qv", "kat_divergent",
+                                  "grid_50_5", "seeded_guess"])
+def test_bicgstab_graph_loop_equals_host_loop(gs, name, monkeypatch):
+    """From its second BiCGStab solve on, a handle runs the iteration loop as a CUDA graph (a
+    while node ended by the kernel that decides the stop); the first solve and MCR_NO_GRAPH use
+    host-polled batches. Same kernels, same order: identical bits, outcome and counts, also
+    for breakdowns and iteration caps."""
+    m, b = system(name)
+    runs = []
+    for env in (None, None, None, "1"):
+        if env:
+            monkeypatch.setenv("MCR_NO_GRAPH", env)
+        dm = gs.DeviceMatrix(m, 0, 5) if env or not runs else runs_dm
+        if not runs:
+            runs_dm = dm
+        for max_it in (10_000, 3):
+            rc, x, rep = dm.solve("bicgstab", b, None, 1e-10, max_it)
+            runs.append((max_it, rc, int(rep.iterations), int(rep.breakdown_which),
+                         float(rep.residual_inf).hex(), x.tobytes()))
+        if env:
+            dm.close()
+    runs_dm.close()
+    by_cap = {}
+    for r in runs:
+        by_cap.setdefault(r[0], []).append(r[1:])
+    for cap, rs in by_cap.items():
+        assert all(r == rs[0] for r in rs), (name, cap)
