@@ -216,7 +216,7 @@ struct BatchPlan {
 };
 
 // ---------------------------------------------------------------- graph mode
-constexpr int GRAPH_UNROLL_BICG = 2;    // iterations per while-body
+constexpr int GRAPH_UNROLL_BICG = 4;    // iterations per while-body (1: 10.51, 2: 10.33, 4: 10.29 ms at C2)
 // One GPU, BiCGStab: the iteration loop is a CUDA graph holding one while node whose body is
 // `unroll` iterations, captured once per handle. The kernel that takes the stop decision sets
 // the node's condition (graph_continue), so the loop ends on the device: no host round trips
