@@ -59,16 +59,27 @@ __device__ __forceinline__ unsigned long long dsmem_load<unsigned long long>(con
     return v;
 }
 
+// A one-CTA system needs no cross-SM ordering at all: __syncthreads orders its global
+// accesses for the whole block, the L1 stays coherent, and no release fence is paid.
 template <bool CL>
 struct SmallSync {
     __device__ __forceinline__ void sync() {
-        if constexpr (CL) cluster_barrier();
-        else cg::this_grid().sync();
+        if constexpr (CL) {
+            if (gridDim.x == 1) __syncthreads();
+            else cluster_barrier();
+        } else {
+            cg::this_grid().sync();
+        }
     }
     template <class T>
     __device__ __forceinline__ T gather(const T* p) const {
-        if constexpr (CL) return __ldcg(p);
+        if constexpr (CL) return gridDim.x == 1 ? *p : __ldcg(p);
         else return *p;
+    }
+    __device__ __forceinline__ void exit_sync() {  // no CTA leaves while others read its slots
+        if constexpr (CL) {
+            if (gridDim.x > 1) cluster_barrier();
+        }
     }
 };
 
@@ -215,7 +226,7 @@ __global__ void __launch_bounds__(SM_NT) k_jacobi_small(Csr R, Vecs V, SolveStat
         st->it = it;
         st->stop = stop;
     }
-    if constexpr (CL) cluster_barrier();  // no CTA leaves while others may read its slots
+    bar.exit_sync();
 }
 
 // BiCGStab, whole solve in one launch (solvers.py:450-491), three grid barriers per iteration.
@@ -390,7 +401,7 @@ __global__ void __launch_bounds__(SM_NT) k_bicg_small(Csr A, Vecs V, SolveState*
         st->which = which;
         st->bd_it = bd_it;
     }
-    if constexpr (CL) cluster_barrier();  // no CTA leaves while others may read its slots
+    bar.exit_sync();
 }
 
 }  // namespace mcr
