@@ -1,8 +1,8 @@
 """``python -m paper_1210_6412_b200 <command> ...`` -- the reference CLI with the GPU solvers.
 
 Runs ``mcreach.cli.main`` (``/root/reference/pkg/src/mcreach/cli.py:55-166``) after
-``plugin.install()`` has added ``jacobi-gpu``, ``bicgstab-gpu`` and ``bicgstab-gpu-exact`` to
-``mcreach.solvers.SOLVERS``:
+``plugin.install()`` has added ``jacobi-gpu``, ``bicgstab-gpu``, ``bicgstab-gpu-exact``,
+``jacobi-gpu-par`` and ``bicgstab-gpu-par`` to ``mcreach.solvers.SOLVERS``:
 
 * ``bench --methods jacobi-gpu,bicgstab-gpu ...`` -- the reference's sweep (``run_sweep``,
   ``bench.py:167-202``) writes GPU rows in its own CSV schema; method names are validated

@@ -8,7 +8,10 @@ Every public name here mirrors ``/root/reference/pkg/src/mcreach/solvers.py``:
   ``fn(m, b, config=None) -> SolveResult``, same stopping rules, same exceptions, same
   ``wall_time`` region (after the right-hand-side check, through the final residual);
 * ``residual_inf_norm`` (:123-133) and ``matvec`` (sparse.py:184-191);
-* ``SOLVERS`` (:494-499) with the GPU methods ``jacobi-gpu`` and ``bicgstab-gpu``.
+* ``jacobi_solve_parallel`` (:233-274) / ``bicgstab_solve_parallel`` (:429-447): row shards
+  over ``config.workers`` GPUs;
+* ``SOLVERS`` (:494-499) with the GPU methods ``jacobi-gpu``, ``bicgstab-gpu``,
+  ``bicgstab-gpu-exact``, ``jacobi-gpu-par`` and ``bicgstab-gpu-par``.
 
 The arithmetic runs in libmcr.so (CUDA, sm_100a) behind the C ABI in include/mcr.h; the
 matrix is uploaded once per ``CsrMatrix`` object and cached while that object lives, like
@@ -34,8 +37,8 @@ from .sparse import DimensionMismatch
 __all__ = [
     "SolverConfig", "SolveResult", "SolverError", "ZeroDiagonal", "NotConverged", "Breakdown",
     "DeviceMatrix", "device_matrix", "jacobi_solve", "bicgstab_solve", "bicgstab_solve_exact",
-    "residual_inf_norm",
-    "matvec", "SOLVERS",
+    "jacobi_solve_parallel", "bicgstab_solve_parallel", "parallel_devices",
+    "residual_inf_norm", "matvec", "SOLVERS",
 ]
 
 
@@ -269,13 +272,14 @@ def _empty_result(start: float) -> SolveResult:
     return SolveResult(np.zeros(0), 0, True, 0.0, time.perf_counter() - start)
 
 
-def _solve(method: str, m, b, config, dots: Optional[str] = None) -> SolveResult:
+def _solve(method: str, m, b, config, dots: Optional[str] = None,
+           device: Optional[int] = None) -> SolveResult:
     cfg = config or SolverConfig()
     b = _check_system(m, b)
     start = time.perf_counter()
     if m.n == 0:
         return _empty_result(start)
-    dm = device_matrix(m, int(getattr(cfg, "device", 0) or 0))
+    dm = device_matrix(m, int(getattr(cfg, "device", 0) or 0) if device is None else device)
     x0 = _initial_guess(m.n, cfg)
     with dm.lock:
         rc, x, rep = dm.solve(method, b, x0, cfg.tolerance, cfg.max_iterations,
@@ -355,8 +359,66 @@ def matvec(m, x) -> np.ndarray:
         return dm.matvec(x)
 
 
+def parallel_devices(n: int, cfg) -> list:
+    """Devices of a row-sharded solve: ``cfg.workers`` GPUs (default: every visible GPU),
+    at most one per row, starting at ``cfg.device`` -- the GPU analogue of the reference's
+    ``resolved_workers`` + ``_row_blocks`` (solvers.py:98-99,159-168). ``MCR_GPU_DEVICES``
+    (comma-separated ordinals, repeats allowed) overrides the choice, e.g. ``0,0`` runs two
+    shards on one GPU."""
+    env = os.environ.get("MCR_GPU_DEVICES")
+    if env:
+        devs = [int(d) for d in env.split(",") if d.strip()]
+        if not devs:
+            raise ValueError("MCR_GPU_DEVICES lists no device")
+        return devs[:max(1, min(len(devs), n))]
+    count = _lib.device_count()
+    if count < 1:
+        raise _lib.NativeLibraryError("no CUDA device visible")
+    workers = cfg.workers if cfg.workers is not None else count
+    k = max(1, min(workers, count, n))
+    dev0 = int(getattr(cfg, "device", 0) or 0)
+    return [(dev0 + i) % count for i in range(k)]
+
+
+def _solve_parallel(method: str, m, b, config) -> SolveResult:
+    cfg = config or SolverConfig()
+    b = _check_system(m, b)
+    start = time.perf_counter()
+    if m.n == 0:
+        return _empty_result(start)
+    if getattr(cfg, "dot_products", "tree") == "sequential":
+        # the reference's sequential dots are one chain over all rows: one GPU
+        return _solve(method, m, b, cfg, dots="sequential")
+    devices = parallel_devices(int(m.n), cfg)
+    from .dist import shard_rows, solve_local_group
+    while len(devices) > 1 and shard_rows(int(m.n), len(devices), len(devices) - 1)[1] < 1:
+        devices = devices[:-1]  # ceil(n/k) blocks: every shard must hold rows
+    if len(devices) == 1:
+        return _solve(method, m, b, cfg, device=devices[0])
+    result, _ = solve_local_group(method, m, b, len(devices), cfg, devices=devices)
+    return SolveResult(result.x, result.iterations, result.converged, result.residual_inf,
+                       time.perf_counter() - start)
+
+
+def jacobi_solve_parallel(m, b, config: Optional[SolverConfig] = None) -> SolveResult:
+    """Row-sharded Jacobi over ``config.workers`` GPUs (solvers.py:233-274 semantics): one
+    contiguous row block per GPU, the iterate exchanged every sweep, the stop test decided
+    identically on every shard. Iterates are bit-identical to ``jacobi_solve``, as the
+    reference's row-block variant is to its sequential one."""
+    return _solve_parallel("jacobi", m, b, config)
+
+
+def bicgstab_solve_parallel(m, b, config: Optional[SolverConfig] = None) -> SolveResult:
+    """Row-sharded BiCGStab over ``config.workers`` GPUs (solvers.py:429-447): p and s
+    exchanged before each product, every inner product reduced per shard and then summed in
+    ascending shard order, identically on all shards."""
+    return _solve_parallel("bicgstab", m, b, config)
+
+
 SOLVERS: dict[str, Callable[..., SolveResult]] = {
     "jacobi-gpu": jacobi_solve,
     "bicgstab-gpu": bicgstab_solve,
     "bicgstab-gpu-exact": bicgstab_solve_exact,
+    "jacobi-gpu-par": jacobi_solve_parallel,
+    "bicgstab-gpu-par": bicgstab_solve_parallel,
 }

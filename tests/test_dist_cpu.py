@@ -192,3 +192,17 @@ def test_row_block_exchange_semantics_gloo(name, world):
         assert abs(int(bic[r][0]) - eb["iterations"]) <= 1
         err = np.max(np.abs(bic[r][1:] - eb["x"])) / max(1.0, np.max(np.abs(eb["x"])))
         assert err <= 1e-9
+
+
+def test_registry_parallel_device_choice(monkeypatch):
+    """SOLVERS' row-sharded drop-ins: MCR_GPU_DEVICES picks the shard devices (repeats allowed,
+    at most one shard per row); the names mirror the reference's jacobi-par / bicgstab-par."""
+    from paper_1210_6412_b200 import solvers as gs
+    assert {"jacobi-gpu-par", "bicgstab-gpu-par"} <= set(gs.SOLVERS)
+    monkeypatch.setenv("MCR_GPU_DEVICES", "0,0,1")
+    assert gs.parallel_devices(100, gs.SolverConfig()) == [0, 0, 1]
+    assert gs.parallel_devices(2, gs.SolverConfig()) == [0, 0]
+    monkeypatch.setenv("MCR_GPU_DEVICES", ",")
+    import pytest
+    with pytest.raises(ValueError):
+        gs.parallel_devices(10, gs.SolverConfig())

@@ -229,3 +229,72 @@ def test_sharded_staged_layout_in_use(mods, monkeypatch):
 def test_fused_p2p_c2(mods):
     check(mods, "jacobi", "c2_trial0", 4, p2p=True)
     check(mods, "bicgstab", "c2_trial0", 4, iter_slack=6, p2p=True)
+
+
+# ---- the registry's row-sharded drop-ins (SOLVERS["jacobi-gpu-par" / "bicgstab-gpu-par"]),
+# the GPU analogue of jacobi_solve_parallel / bicgstab_solve_parallel (S/solvers.py:233-274,
+# 429-447). MCR_GPU_DEVICES places several shards on the one GPU of this box.
+def run_registry(mods, method, name, devices, monkeypatch):
+    dist, gs = mods
+    monkeypatch.setenv("MCR_GPU_DEVICES", devices)
+    m, b = system(name)
+    exp = expected(name, method)
+    c = exp["config"]
+    conf = gs.SolverConfig(tolerance=c["tolerance"], max_iterations=c["max_iterations"],
+                           guess_seed=c["guess_seed"])
+    fn = gs.SOLVERS[f"{method}-gpu-par"]
+    try:
+        return exp, "ok", fn(m, b, conf), None
+    except gs.NotConverged as err:
+        return exp, "not_converged", err.result, err
+    except gs.Breakdown as err:
+        return exp, "breakdown", err.result, err
+    except gs.ZeroDiagonal as err:
+        return exp, "zero_diagonal", None, err
+
+
+@pytest.mark.parametrize("devices", ["0", "0,0", "0,0,0"])
+@pytest.mark.parametrize("name", ["c1_seed77", "c4_2000_3999", "chain_random1", "seeded_guess",
+                                  "dense_1024"] + KATS)
+@pytest.mark.parametrize("method", ["jacobi", "bicgstab"])
+def test_registry_parallel_methods(mods, method, name, devices, monkeypatch):
+    exp, outcome, res, err = run_registry(mods, method, name, devices, monkeypatch)
+    m, _ = system(name)
+    assert outcome == exp["outcome"], (name, devices, outcome, exp["outcome"])
+    if outcome == "zero_diagonal":
+        assert err.index == exp["zero_index"]
+        return
+    stride = manifest()["sample_stride"]
+    ref_x = exp["x"] if exp["x"] is not None else exp["x_sample"]
+    got_x = res.x if exp["x"] is not None else res.x[::stride]
+    assert res.x.shape == (m.n,) and res.wall_time > 0.0
+    if outcome == "breakdown":
+        assert err.which == exp["which"] and err.iteration == exp["breakdown_iteration"]
+    if method == "jacobi":  # bit-identical to the reference at every shard count
+        assert res.iterations == exp["iterations"]
+        assert np.array_equal(got_x, ref_x)
+        assert float(res.residual_inf).hex() == exp["residual_inf"]
+    else:
+        assert abs(res.iterations - exp["iterations"]) <= 1
+        if outcome == "ok":
+            assert rel_err(got_x, ref_x) <= REL_TOL
+
+
+def test_registry_parallel_workers_clamped(mods, monkeypatch):
+    """Without MCR_GPU_DEVICES the shard count is min(workers, visible GPUs, n); one GPU
+    runs the plain single-device solve (same bits)."""
+    dist, gs = mods
+    monkeypatch.delenv("MCR_GPU_DEVICES", raising=False)
+    from paper_1210_6412_b200 import _lib
+    count = _lib.device_count()
+    assert gs.parallel_devices(10, gs.SolverConfig(workers=64)) == list(range(min(count, 10)))
+    assert gs.parallel_devices(1, gs.SolverConfig()) == [0]
+    m, b = system("c4_2000_3999")
+    one = gs.SOLVERS["jacobi-gpu"](m, b)
+    par = gs.SOLVERS["jacobi-gpu-par"](m, b, gs.SolverConfig(workers=8))
+    assert par.iterations == one.iterations and np.array_equal(par.x, one.x)
+    from paper_1210_6412_b200.sparse import CsrMatrix
+    empty = gs.SOLVERS["bicgstab-gpu-par"](CsrMatrix(0, np.zeros(1, np.int64),
+                                                     np.zeros(0, np.int64), np.zeros(0)),
+                                           np.zeros(0))
+    assert empty.converged and empty.iterations == 0

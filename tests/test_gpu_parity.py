@@ -336,7 +336,8 @@ def test_plugin_registers_into_reference():
     from paper_1210_6412_b200 import plugin
     reg = {}
     added = plugin.install(reg)
-    assert set(added) == {"jacobi-gpu", "bicgstab-gpu", "bicgstab-gpu-exact"}
+    assert set(added) == {"jacobi-gpu", "bicgstab-gpu", "bicgstab-gpu-exact", "jacobi-gpu-par",
+                          "bicgstab-gpu-par"}
     from mcreach import GenSpec, generate_dd_matrix, generate_rhs
     from mcreach.solvers import NotConverged, SolveResult, SolverConfig
     m = generate_dd_matrix(GenSpec(n=300, nnz=3000, seed=3))
