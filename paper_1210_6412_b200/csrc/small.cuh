@@ -111,32 +111,68 @@ __device__ __forceinline__ void load_tile(const Csr& A, int t, SmallSmem& sm) {
 // at once, then thread r adds its row left to right. G uses plain (L1-cached) loads: within a
 // phase the gathered vectors are read-only, and the grid barrier between phases is a
 // gpu-scope fence, which invalidates L1 (so the next phase never sees a stale line).
+// tile_products issues all of a thread's gathers before the first product (one L2 round trip
+// per phase instead of one per unrolled group); the caller syncs the CTA before tile_chain.
+constexpr int SM_PER = (TILE_NNZ + SM_NT - 1) / SM_NT;  // entries per thread of a cached tile
+
 template <class Gather>
-__device__ __forceinline__ double tile_rowsum(const Csr& A, SmallSmem& sm, Gather G) {
+__device__ __forceinline__ void tile_products(SmallSmem& sm, Gather G) {
+    const int tid = threadIdx.x;
+    const int len = (int)(sm.e1 - sm.e0);
+    if (len <= SM_NT * (SM_PER / 2)) {  // short tile (Table-1 shapes): the plain loop is cheaper
+        for (int k = tid; k < len; k += SM_NT) sm.prod[k] = dmul(sm.val[k], G(sm.col[k]));
+        return;
+    }
+    double g[SM_PER];
+#pragma unroll
+    for (int u = 0; u < SM_PER; ++u) {
+        const int k = tid + u * SM_NT;
+        g[u] = k < len ? G(sm.col[k]) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < SM_PER; ++u) {
+        const int k = tid + u * SM_NT;
+        if (k < len) sm.prod[k] = dmul(sm.val[k], g[u]);
+    }
+}
+
+__device__ __forceinline__ double tile_chain(const SmallSmem& sm) {
     const int tid = threadIdx.x;
     double acc = 0.0;
-    if (sm.cached) {
-        const int len = (int)(sm.e1 - sm.e0);
-        for (int k = tid; k < len; k += SM_NT) sm.prod[k] = dmul(sm.val[k], G(sm.col[k]));
-        __syncthreads();
-        if (tid < sm.nrows) {
-            const int b = sm.rp[tid], e = sm.rp[tid + 1];
-            for (int k = b; k < e; ++k) acc = dadd(acc, sm.prod[k]);
-        }
-        __syncthreads();
-    } else {  // one long row
-        double a = 0.0;
-        for (long long b0 = sm.e0; b0 < sm.e1; b0 += TILE_NNZ) {
-            const int clen = (int)((sm.e1 - b0) < TILE_NNZ ? (sm.e1 - b0) : TILE_NNZ);
-            for (int k = tid; k < clen; k += SM_NT)
-                sm.prod[k] = dmul(A.val[b0 + k], G(A.col[b0 + k]));
-            __syncthreads();
-            if (tid == 0)
-                for (int k = 0; k < clen; ++k) a = dadd(a, sm.prod[k]);
-            __syncthreads();
-        }
-        acc = a;
+    if (tid < sm.nrows) {
+        const int b = sm.rp[tid], e = sm.rp[tid + 1];
+        for (int k = b; k < e; ++k) acc = dadd(acc, sm.prod[k]);
     }
+    return acc;
+}
+
+// Streamed row longer than a tile (sm.cached == 0): thread 0 adds it chunk by chunk.
+template <class Gather>
+__device__ __forceinline__ double long_row_sum(const Csr& A, SmallSmem& sm, Gather G) {
+    const int tid = threadIdx.x;
+    double a = 0.0;
+    for (long long b0 = sm.e0; b0 < sm.e1; b0 += TILE_NNZ) {
+        const int clen = (int)((sm.e1 - b0) < TILE_NNZ ? (sm.e1 - b0) : TILE_NNZ);
+        for (int k = tid; k < clen; k += SM_NT)
+            sm.prod[k] = dmul(A.val[b0 + k], G(A.col[b0 + k]));
+        __syncthreads();
+        if (tid == 0)
+            for (int k = 0; k < clen; ++k) a = dadd(a, sm.prod[k]);
+        __syncthreads();
+    }
+    return a;
+}
+
+// (BiCGStab's gathers read three vectors each: the plain loop keeps fewer loads in flight but
+// measured faster there than tile_products, C4 -3..-8%)
+template <class Gather>
+__device__ __forceinline__ double tile_rowsum(const Csr& A, SmallSmem& sm, Gather G) {
+    if (!sm.cached) return long_row_sum(A, sm, G);
+    const int len = (int)(sm.e1 - sm.e0);
+    for (int k = threadIdx.x; k < len; k += SM_NT) sm.prod[k] = dmul(sm.val[k], G(sm.col[k]));
+    __syncthreads();
+    const double acc = tile_chain(sm);
+    __syncthreads();
     return acc;
 }
 
@@ -191,11 +227,22 @@ __global__ void __launch_bounds__(SM_NT) k_jacobi_small(Csr R, Vecs V, SolveStat
     if (row >= 0) { bi = V.b[row]; di = V.d[row]; xi = V.x_jac0[row]; }
     long long it = 0;
     int stop = RUNNING;
+    const bool cached = sm.cached;
+    // products of sweep 1 (x0 buffer); from then on the next sweep's products are formed right
+    // after each barrier, while the stop test's max is still in flight (speculative: a sweep
+    // that is never run only wrote shared memory)
+    if (cached) tile_products(sm, [&](int c) { return bar.gather(V.x_jac0 + c); });
     while (stop == RUNNING) {
         ++it;
         const double* xin = (it & 1) ? V.x_jac0 : V.x_jac1;
         double* xout = (it & 1) ? V.x_jac1 : V.x_jac0;
-        const double s = tile_rowsum(R, sm, [&](int c) { return bar.gather(xin + c); });
+        double s;
+        if (cached) {
+            __syncthreads();
+            s = tile_chain(sm);
+        } else {
+            s = long_row_sum(R, sm, [&](int c) { return bar.gather(xin + c); });
+        }
         unsigned long long mb = 0;
         if (row >= 0) {
             const double xn = ddiv(dsub(bi, s), di);   // (b - R x) / d
@@ -203,22 +250,25 @@ __global__ void __launch_bounds__(SM_NT) k_jacobi_small(Csr R, Vecs V, SolveStat
             mb = absbits(dsub(xn, xi));
             xi = xn;
         }
-        mb = group_max<SM_NT / 32, 0>(mb, sm.redu);
-        double md;
+        mb = group_max<SM_NT / 32, 0>(mb, sm.redu);  // (its barrier also ends the chains' reads)
+        unsigned long long mraw;
         if constexpr (CL) {
             // slot it&1 is rewritten two sweeps later, after every CTA has passed the barrier
             // that follows its reads
             if (threadIdx.x == 0) sm.mx[it & 1] = mb;
             bar.sync();
-            md = cluster_read_max(&sm.mx[it & 1], (int)gridDim.x);
+            mraw = 0;
+            for (int k = 0; k < (int)gridDim.x; ++k) mraw = umax(mraw, dsmem_load(&sm.mx[it & 1], k));
         } else {
             if (threadIdx.x == 0 && mb) atomicMax(&maxslot[it % 3], mb);
             // slot (it+1)%3 was last read before the previous barrier by every CTA: clear it for
             // the next sweep before this barrier, so no CTA can add to it before it is cleared
             if (blockIdx.x == 0 && threadIdx.x == 0) maxslot[(it + 1) % 3] = 0ull;
             bar.sync();
-            md = read_max(&maxslot[it % 3]);
+            mraw = __ldcg(&maxslot[it % 3]);
         }
+        if (cached) tile_products(sm, [&](int c) { return bar.gather(xout + c); });
+        const double md = bits2d(mraw);
         if (md <= tol) stop = CONVERGED;
         else if (it >= max_it) stop = NOTCONV;
     }
