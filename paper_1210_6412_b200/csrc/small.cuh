@@ -193,17 +193,21 @@ __device__ __forceinline__ double read_max(unsigned long long* slot) {
     return bits2d(__ldcg(slot));
 }
 
-// all_reduce_partials over the CTAs' shared-memory slots of one cluster: the same operations
-// in the same order (0.0 + P[k] per thread, then the CTA tree), so the same bits.
-__device__ __forceinline__ double cluster_reduce_partials(const double* slot, int count, double* red) {
-    double acc = 0.0;
-    for (int k = threadIdx.x; k < count; k += SM_NT) acc = dadd(acc, dsmem_load(slot, k));
-    acc = group_sum<SM_NT / 32, 0>(acc, red);
-    if (threadIdx.x == 0) red[0] = acc;
-    __syncthreads();
-    acc = red[0];
-    __syncthreads();
-    return acc;
+// The same value for count <= 32 without the CTA tree or any __syncthreads: every warp loads
+// the partials into lanes 0..count-1 and runs group_sum's warp tree. In group_sum those lanes
+// of warp 0 are the only nonzero inputs; the other warps' sums are +0.0 and the second-level
+// tree adds them to warp 0's sum, which is never -0.0 (each input is 0.0 + P, and a sum of
+// values other than -0.0 is never -0.0 in round-to-nearest), so adding them changes nothing:
+// same bits as all_reduce_partials (the grid variant) over the CTAs' shared-memory slots.
+// One CTA: the tree of a single nonzero input is 0.0 + P itself.
+__device__ __forceinline__ double cluster_allreduce(const double* slot, int count) {
+    if (count == 1) return dadd(0.0, *slot);
+    const unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    double v = lane < count ? dadd(0.0, dsmem_load(slot, lane)) : 0.0;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v = dadd(v, __shfl_down_sync(full, v, off));
+    return __shfl_sync(full, v, 0);
 }
 __device__ __forceinline__ double cluster_read_max(const unsigned long long* slot, int count) {
     unsigned long long m = 0;
@@ -290,7 +294,7 @@ __global__ void __launch_bounds__(SM_NT) k_jacobi_small(Csr R, Vecs V, SolveStat
 // separate slots (parts + k*pstride: q.v, t.t, t.s, q.r) because no barrier separates a
 // slot's all-reduce from the next slot's writes. maxslot[2] zero on entry.
 template <bool CL>
-__global__ void __launch_bounds__(SM_NT) k_bicg_small(Csr A, Vecs V, SolveState* st,
+__global__ void __launch_bounds__(SM_NT, 1) k_bicg_small(Csr A, Vecs V, SolveState* st,
                                                       unsigned long long* maxslot, double* parts,
                                                       int pstride) {
     __shared__ SmallSmem sm;
@@ -312,7 +316,7 @@ __global__ void __launch_bounds__(SM_NT) k_bicg_small(Csr A, Vecs V, SolveState*
         }
     };
     auto allreduce = [&](int k, const double* gslot) {
-        if constexpr (CL) return cluster_reduce_partials(&sm.part[k], nt, sm.red);
+        if constexpr (CL) return cluster_allreduce(&sm.part[k], nt);  // nt <= 16
         else return all_reduce_partials(gslot, nt, sm.red);
     };
     auto publish_max = [&](int k, unsigned long long m) {  // m valid in thread 0
