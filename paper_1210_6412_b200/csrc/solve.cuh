@@ -87,7 +87,9 @@ void launch_mv(mcr_matrix* h, bool offdiag, const double* x, const Vecs& V, int6
 
 template <int PH>
 void launch_phase(mcr_matrix* h, const Vecs& V, int64_t* launches) {
-    launch_pdl(k_phase<PH>, h->nchunks(), CHUNK_NT, 0, h->stream, V, (int)h->n, h->st);
+    constexpr int rows = CHUNK_NT * phase_per<PH>();
+    const int grid = PH == PH_E ? h->nchunks() : (int)((h->n + rows - 1) / rows);
+    launch_pdl(k_phase<PH>, grid, CHUNK_NT, 0, h->stream, V, (int)h->n, h->st);
     ++*launches;
 }
 

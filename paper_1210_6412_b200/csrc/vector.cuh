@@ -12,14 +12,24 @@ namespace mcr {
 // stopped solve is made harmless: p and s are dead once the solve has stopped (only x and the
 // state are read afterwards), so A and C write them unconditionally and C adds to the running
 // max only while live; E rewrites x with its old value and skips its scalar step.
+// Rows per thread: A and C (no inner product, so no summation order to keep) take
+// MCR_PHASE_PER_AC rows so their grid fits in one wave of co-resident CTAs; E keeps CHUNK_PER
+// because its per-CTA q.r partials fix the dot order.
+#ifndef MCR_PHASE_PER_AC
+#define MCR_PHASE_PER_AC 8
+#endif
+template <int PH>
+__host__ __device__ constexpr int phase_per() { return PH == PH_E ? CHUNK_PER : MCR_PHASE_PER_AC; }
+
 template <int PH>
 __global__ void __launch_bounds__(CHUNK_NT) k_phase(Vecs V, int n, SolveState* st) {
+    constexpr int CHUNK_PER = phase_per<PH>();
     __shared__ double s_red[CHUNK_NT / 32];
     __shared__ unsigned long long s_redu[CHUNK_NT / 32];
     __shared__ int s_flag;
     griddep_wait();
     griddep_launch();
-    const int base = blockIdx.x * CHUNK_ROWS + threadIdx.x;
+    const int base = blockIdx.x * (CHUNK_NT * CHUNK_PER) + threadIdx.x;
     if constexpr (PH == PH_A) {
         const double beta = st->beta, w = st->w;
         double r[CHUNK_PER], p[CHUNK_PER], v[CHUNK_PER];
