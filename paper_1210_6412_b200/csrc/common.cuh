@@ -82,6 +82,27 @@ struct TileDesc {
     int r0, r1;
 };
 
+// The stage's tile id and descriptor as read by lane 0 and broadcast: only the thread that
+// releases the stage (lane 0's mbarrier arrive) reads the producer-written slots, so the
+// producer's next write of them is ordered after that read by the arrive/wait pair alone.
+__device__ __forceinline__ int stage_tile(const int* s_tile, const TileDesc* s_desc, int s,
+                                          TileDesc& d) {
+    const unsigned full = 0xffffffffu;
+    int t = 0;
+    long long e0 = 0, e1 = 0;
+    int r0 = 0, r1 = 0;
+    if ((threadIdx.x & 31) == 0) {
+        t = s_tile[s];
+        if (t >= 0) { e0 = s_desc[s].e0; e1 = s_desc[s].e1; r0 = s_desc[s].r0; r1 = s_desc[s].r1; }
+    }
+    t = __shfl_sync(full, t, 0);
+    d.e0 = __shfl_sync(full, e0, 0);
+    d.e1 = __shfl_sync(full, e1, 0);
+    d.r0 = __shfl_sync(full, r0, 0);
+    d.r1 = __shfl_sync(full, r1, 0);
+    return t;
+}
+
 struct Csr {
     const long long* rp;
     const int* col;

@@ -116,14 +116,14 @@ __global__ void __launch_bounds__(SP_THREADS, MCR_SP_MINB) k_spmv(Csr A, const d
         for (int i = 0;; ++i) {
             const int s = i % SP_STAGES;
             mbar_wait(&full_bar[s], (uint32_t)((i / SP_STAGES) & 1));
-            const int t = s_tile[s];
+            TileDesc d;
+            const int t = stage_tile(s_tile, s_desc, s, d);
             if (t < 0) break;
             if (stopped) {  // the solve has stopped: only release the prefetched stages
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty_bar[s]);
                 continue;
             }
-            const TileDesc d = s_desc[s];
             const int nrows = d.r1 - d.r0;
             const int row = d.r0 + tid;
             EpiIn in{0.0, 0.0, 0.0};

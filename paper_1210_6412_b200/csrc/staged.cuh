@@ -242,9 +242,9 @@ __global__ void __launch_bounds__(SP_THREADS, MCR_SP_MINB) k_spmv_staged(Staged 
         for (int i = 0;; ++i) {
             const int s = i % STG_STAGES;
             mbar_wait(&full_bar[s], (uint32_t)((i / STG_STAGES) & 1));
-            const int t = s_tile[s];
+            TileDesc d;
+            const int t = stage_tile(s_tile, s_desc, s, d);
             if (t < 0) break;
-            const TileDesc d = s_desc[s];
             const int nrows = d.r1 - d.r0;
             const int row = d.r0 + tid;
             EpiIn in{0.0, 0.0, 0.0};

@@ -19,6 +19,11 @@ for name in ("grid_20_9", "c4_667_1333", "kat_breakdown_qv", "dense_1024"):
         dm.solve("bicgstab", b, None, 1e-10, 50, dots="sequential")
         dm.matvec(np.ones(m.n))
         dm.close()
+m, b = system("c1_seed77")  # grid-variant small solvers, long tiles (unrolled speculative gathers)
+dm = solvers.DeviceMatrix(m, 0)
+dm.solve("jacobi", b, None, 1e-10, 30)
+dm.solve("bicgstab", b, None, 1e-10, 5)
+dm.close()
 m, b = system("c4_2000_3999")
 dist.solve_local_group("jacobi", m, b, 2)
 dist.solve_local_group("bicgstab", m, b, 2)
