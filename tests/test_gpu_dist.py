@@ -298,3 +298,19 @@ def test_registry_parallel_workers_clamped(mods, monkeypatch):
                                                      np.zeros(0, np.int64), np.zeros(0)),
                                            np.zeros(0))
     assert empty.converged and empty.iterations == 0
+
+
+def test_registry_parallel_sequential_dots_is_exact(mods, monkeypatch):
+    """bicgstab-gpu-par with the reference's sequential inner products runs the one-GPU exact
+    mode (one chain over all rows): bit-identical to the reference's bicgstab."""
+    dist, gs = mods
+    monkeypatch.setenv("MCR_GPU_DEVICES", "0,0")
+    name = "c4_2000_3999"
+    m, b = system(name)
+    exp = expected(name, "bicgstab")
+    c = exp["config"]
+    conf = gs.SolverConfig(tolerance=c["tolerance"], max_iterations=c["max_iterations"],
+                           guess_seed=c["guess_seed"], dot_products="sequential")
+    got = gs.SOLVERS["bicgstab-gpu-par"](m, b, conf)
+    assert got.iterations == exp["iterations"]
+    assert sha(got.x) == exp["x_sha256"]
