@@ -348,18 +348,27 @@ int bicgstab_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double t
     const bool sh = h->sharded();
     double* p_full = h->vec(V_P);
     double* s_full = h->vec(V_S);
-    // the graph is built on the second BiCGStab solve of a handle: capture + instantiation
-    // cost about as much as a solve's host round trips save, so a handle used once (the
-    // end-to-end path) keeps the host-batched loop
-    const bool use_graph = graph_mode(h) && !h->seqdots && max_it >= 1 && h->bicg_solves++ >= 1;
+    auto body = [&](int64_t* n) {
+        launch_phase<PH_A>(h, V, n);               // p = r + beta (p - w v)
+        launch_mv<EPI_V>(h, false, p_full, V, n);  // v = M p, q.v -> a
+        launch_phase<PH_C>(h, V, n);               // s = r - a v, max|s|
+        launch_mv<EPI_T>(h, false, s_full, V, n);  // t = M s, t.t, t.s -> w
+        launch_phase<PH_E>(h, V, n);               // x, r updates, q.r -> beta; loop condition
+    };
+    // From the second BiCGStab solve of a handle the loop is the graph from the start. On the
+    // first solve of a large system (the end-to-end path uploads a fresh matrix per step) the
+    // graph is captured and instantiated on the host while the first host-issued batch runs on
+    // the device, and takes over from the next iteration on; for small systems capture +
+    // instantiation cost more than the batch hides, so they keep the host-batched loop.
+    const bool gmode = graph_mode(h) && !h->seqdots && max_it >= 1;
+    const bool first = h->bicg_solves++ == 0;
+    const bool use_graph = gmode && !first;
     if (use_graph && !h->gl_bicg.exec && !h->gl_bicg.failed)
-        TRY(build_graph_loop(h, h->gl_bicg, GRAPH_UNROLL_BICG, [&](int64_t* n) {
-            launch_phase<PH_A>(h, V, n);               // p = r + beta (p - w v)
-            launch_mv<EPI_V>(h, false, p_full, V, n);  // v = M p, q.v -> a
-            launch_phase<PH_C>(h, V, n);               // s = r - a v, max|s|
-            launch_mv<EPI_T>(h, false, s_full, V, n);  // t = M s, t.t, t.s -> w
-            launch_phase<PH_E>(h, V, n);               // x, r updates, q.r -> beta; loop condition
-        }));
+        TRY(build_graph_loop(h, h->gl_bicg, GRAPH_UNROLL_BICG, body));
+    long long late_min_nnz = 2000000;  // C2 has 1e7
+    if (const char* env = std::getenv("MCR_LATE_GRAPH_MIN_NNZ")) late_min_nnz = std::atoll(env);
+    bool late_graph = gmode && first && !h->gl_bicg.exec && !h->gl_bicg.failed &&
+                      (long long)h->nnz >= late_min_nnz;
     const bool graph = use_graph && h->gl_bicg.exec;
     set_state(h, tol, max_it);
     if (graph) h->h_st->cond = h->gl_bicg.cond;
@@ -393,6 +402,7 @@ int bicgstab_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double t
             TRY(read_state(h));
         }
     }
+    if (late_graph) batch = 8;  // enough device work to hide the capture
     while (!h->h_st->stop && iters < max_it) {
         const int k = (int)std::min<int64_t>(batch, max_it - iters);
         for (int i = 0; i < k; ++i) {
@@ -412,6 +422,24 @@ int bicgstab_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double t
         }
         CK(cudaGetLastError());
         iters += k;
+        if (late_graph) {  // host work while the batch runs
+            late_graph = false;
+            TRY(build_graph_loop(h, h->gl_bicg, GRAPH_UNROLL_BICG, body));
+            TRY(read_state(h));
+            if (h->gl_bicg.exec && !h->h_st->stop && iters < max_it) {
+                const long long it0 = h->h_st->it;
+                h->h_st->cond = h->gl_bicg.cond;
+                CK(cudaMemcpyAsync(&h->st->cond, &h->h_st->cond, sizeof(h->h_st->cond),
+                                   cudaMemcpyHostToDevice, h->stream));
+                CK(cudaGraphLaunch(h->gl_bicg.exec, h->stream));
+                TRY(read_state(h));
+                const int U = h->gl_bicg.unroll;
+                launched += 5 * ((h->h_st->it - it0 + U) / U * U);
+                break;
+            }
+            batch = std::min(batch * 2, 32);
+            continue;
+        }
         TRY(read_state(h));
         batch = std::min(batch * 2, 32);
     }

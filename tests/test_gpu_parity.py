@@ -400,3 +400,29 @@ def test_bicgstab_graph_loop_equals_host_loop(gs, name, monkeypatch):
         by_cap.setdefault(r[0], []).append(r[1:])
     for cap, rs in by_cap.items():
         assert all(r == rs[0] for r in rs), (name, cap)
+
+
+@pytest.mark.parametrize("name", ["c2_trial0", "c1_seed77", "kat_breakdown_qv", "kat_divergent",
+                                  "grid_50_5", "seeded_guess"])
+def test_bicgstab_late_graph_equals_host_loop(gs, name, monkeypatch):
+    """The first BiCGStab solve of a large handle captures the graph while its first batch of
+    8 iterations runs and hands the rest of the loop to it (MCR_LATE_GRAPH_MIN_NNZ=0 forces
+    that for every size): identical bits, outcome and counts to the host-polled loop, for
+    stops inside the batch (iteration caps 3 and 8), right after it (9) and later."""
+    m, b = system(name)
+    got = {}
+    for env in ("late", "host"):
+        monkeypatch.delenv("MCR_NO_GRAPH", raising=False)
+        monkeypatch.setenv("MCR_LATE_GRAPH_MIN_NNZ", "0")
+        if env == "host":
+            monkeypatch.setenv("MCR_NO_GRAPH", "1")
+        for max_it in (10_000, 3, 8, 9):
+            dm = gs.DeviceMatrix(m, 0, 5)  # fresh handle: its first solve
+            try:
+                rc, x, rep = dm.solve("bicgstab", b, None, 1e-10, max_it)
+            finally:
+                dm.close()
+            got.setdefault(max_it, []).append((rc, int(rep.iterations), int(rep.breakdown_which),
+                                               float(rep.residual_inf).hex(), x.tobytes()))
+    for max_it, (late, host) in got.items():
+        assert late == host, (name, max_it)
