@@ -112,12 +112,28 @@ MCR_API int mcr_matrix_create(int64_t n, const int64_t* rstart, const int64_t* c
 MCR_API void mcr_matrix_destroy(mcr_matrix* m);
 MCR_API int mcr_matrix_info_get(const mcr_matrix* m, mcr_matrix_info* info);
 
-/* Inner products of BiCGStab: TREE (default) = deterministic fixed-shape tree reductions,
- * fused into the producing kernels; SEQUENTIAL = the reference's strictly left-to-right
- * _dot_ascending (solvers.py:136-141), bit-identical to the reference and much slower (one
- * dependent add per element). Jacobi, SpMV and the residual are bit-identical in both modes. */
-enum { MCR_DOTS_TREE = 0, MCR_DOTS_SEQUENTIAL = 1 };
+/* Inner products of BiCGStab. SEQUENTIAL = the reference's strictly left-to-right
+ * _dot_ascending (solvers.py:136-141), bit-identical to the reference, computed in parallel by
+ * k_xdot (csrc/xdot.cuh: binade runs + candidate tables, checked, with exact fallbacks);
+ * SERIAL = the same bits from one dependent add per element on one CTA (slow; cross-check);
+ * TREE = deterministic fixed-shape trees fused into the producing kernels (not the
+ * reference's order: iteration counts may differ). Jacobi, SpMV and the residual are
+ * bit-identical in every mode. */
+enum { MCR_DOTS_TREE = 0, MCR_DOTS_SEQUENTIAL = 1, MCR_DOTS_SERIAL = 2 };
 MCR_API int mcr_set_dot_mode(mcr_matrix* m, int mode);
+
+/* parallel_dot_products (solvers.py:98, 384-396): with nblocks > 1 every inner product is the
+ * sum, in ascending block order starting from 0.0, of the reference-order dots of the
+ * _row_blocks(n, nblocks) row blocks (solvers.py:159-168). 1 = off. */
+MCR_API int mcr_set_dot_blocks(mcr_matrix* m, int nblocks);
+
+/* Stand-alone reference-order dot on `device` (host arrays): out[0] = the dot (the blocks'
+ * dots summed in ascending order from 0.0 when nblocks > 1), out[1 + b] = block b's dot
+ * (np.cumsum(u * v)[-1] of the block, 0.0 when empty). stats (may be NULL): fallback counters,
+ * filled only when the library runs with MCR_XDOT_STATS=1. Replaces _dot_ascending
+ * (solvers.py:136-141) and _ParOps.dot (solvers.py:384-396). */
+MCR_API int mcr_xdot(int device, int64_t n, const double* u, const double* v, int nblocks,
+                     double* out, uint64_t* stats);
 
 /* Use `stream` (a cudaStream_t on the handle's device, or NULL for the handle's own stream)
  * for every later call on this handle. */

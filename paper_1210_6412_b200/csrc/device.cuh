@@ -4,6 +4,7 @@
 //   spmv.cuh     persistent TMA-pipelined CSR SpMV (k_spmv<EPI>) and SELL-32-sigma
 //   small.cuh    whole-solve cooperative kernels for small systems
 //   vector.cuh   BiCGStab vector phases, reference-order dots, row-shard finalisation
+//   xdot.cuh     the reference's sequential inner product, bit-exact, in parallel
 //   dense.cuh    dense slab GEMV (k_dense<EPI>)
 //   upload.cuh   upload-time kernels
 //   staged.cuh   band-staged two-pass SpMV for x far larger than L2
@@ -13,6 +14,7 @@
 #include "spmv.cuh"
 #include "small.cuh"
 #include "vector.cuh"
+#include "xdot.cuh"
 #include "dense.cuh"
 #include "upload.cuh"
 #include "staged.cuh"

@@ -83,6 +83,9 @@ enum { V_X = 0, V_X1, V_P, V_S, V_FULL_COUNT, V_B = V_FULL_COUNT, V_R, V_Q, V_V,
 }  // namespace
 
 struct mcr_matrix;
+namespace {
+struct XdotCtx;  // xdot_host.cuh
+}
 
 // A Markov chain with its goal set and the reduced system built from it (chain.cuh).
 struct mcr_chain {
@@ -186,7 +189,9 @@ struct mcr_matrix {
     SolveState* h_st = &h_state;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int64_t bytes = 0;
-    int seqdots = 0;
+    int seqdots = 0;       // 0 tree dots, 1 reference order (k_xdot), 2 reference order, serial
+    int dot_blocks = 1;    // > 1: parallel_dot_products over that many row blocks
+    XdotCtx* xdot = nullptr;
     // graph mode (solve.cuh): the whole iteration loop as one CUDA graph with a while node
     struct GraphLoop {
         cudaGraphExec_t exec = nullptr;

@@ -9,6 +9,7 @@
 // memory, so the host only enqueues batches of iterations and polls the stop flag once per
 // batch.
 #include "handle.h"
+#include "xdot_host.cuh"
 #include "storage.cuh"
 #include "solve.cuh"
 #include "chain_host.cuh"
@@ -50,6 +51,8 @@ MCR_API void mcr_matrix_destroy(mcr_matrix* h) {
                 if (p) cudaFreeAsync(p, s);
             cudaStreamSynchronize(s);
         }
+        xdot_free(h->xdot, s ? s : h->stream);
+        h->xdot = nullptr;
         for (auto* gl : {&h->gl_bicg}) {
             if (gl->exec) cudaGraphExecDestroy(gl->exec);
             if (gl->graph) cudaGraphDestroy(gl->graph);
@@ -478,12 +481,64 @@ MCR_API int mcr_matrix_info_get(const mcr_matrix* h, mcr_matrix_info* info) {
 
 MCR_API int mcr_set_dot_mode(mcr_matrix* h, int mode) {
     if (!h) return fail(MCR_INVALID_ARGUMENT, "NULL handle");
-    if (mode != MCR_DOTS_TREE && mode != MCR_DOTS_SEQUENTIAL)
+    if (mode != MCR_DOTS_TREE && mode != MCR_DOTS_SEQUENTIAL && mode != MCR_DOTS_SERIAL)
         return fail(MCR_INVALID_ARGUMENT, "unknown dot mode");
     std::lock_guard<std::mutex> lk(h->mu);
-    if (mode == MCR_DOTS_SEQUENTIAL && h->sharded())
+    if (mode != MCR_DOTS_TREE && h->sharded())
         return fail(MCR_INVALID_ARGUMENT, "sequential dots need the whole system on one GPU");
-    h->seqdots = mode == MCR_DOTS_SEQUENTIAL;
+    h->seqdots = mode;
+    return MCR_OK;
+}
+
+MCR_API int mcr_set_dot_blocks(mcr_matrix* h, int nblocks) {
+    if (!h) return fail(MCR_INVALID_ARGUMENT, "NULL handle");
+    if (nblocks < 1) return fail(MCR_INVALID_ARGUMENT, "dot blocks must be >= 1");
+    std::lock_guard<std::mutex> lk(h->mu);
+    h->dot_blocks = nblocks;
+    return MCR_OK;
+}
+
+MCR_API int mcr_xdot(int device, int64_t n, const double* u, const double* v, int nblocks,
+                     double* out, uint64_t* stats) {
+    if (n < 0 || nblocks < 1 || !out || (n > 0 && (!u || !v)))
+        return fail(MCR_INVALID_ARGUMENT, "mcr_xdot: bad arguments");
+    DeviceGuard g(device);
+    cudaStream_t s;
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    struct Cleanup {
+        cudaStream_t s;
+        std::vector<void*> p;
+        XdotCtx* X = nullptr;
+        ~Cleanup() {
+            for (void* q : p) cudaFreeAsync(q, s);
+            xdot_free(X, s);
+            cudaStreamSynchronize(s);
+            cudaStreamDestroy(s);
+        }
+    } c{s, {}};
+    double *du = nullptr, *dv = nullptr, *dout = nullptr;
+    const size_t bytes = sizeof(double) * (size_t)std::max<int64_t>(n, 1);
+    CK(cudaMallocAsync((void**)&du, bytes, s)); c.p.push_back(du);
+    CK(cudaMallocAsync((void**)&dv, bytes, s)); c.p.push_back(dv);
+    CK(cudaMallocAsync((void**)&dout, sizeof(double) * (size_t)(2 + nblocks), s)); c.p.push_back(dout);
+    if (n > 0) {
+        CK(cudaMemcpyAsync(du, u, sizeof(double) * (size_t)n, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(dv, v, sizeof(double) * (size_t)n, cudaMemcpyHostToDevice, s));
+    }
+    c.X = new XdotCtx();
+    TRY(xdot_smem_attr<SQ_TEST>());
+    TRY(xdot_plan(*c.X, SQ_TEST, s, device, n, 1, nblocks, du, dv, nullptr, nullptr));
+    const auto& P = c.X->plan[SQ_TEST];
+    k_xdot<SQ_TEST><<<P.grid, xd::NT, P.smem, s>>>(xdot_args(*c.X, SQ_TEST, dout), nullptr);
+    CK(cudaGetLastError());
+    std::vector<double> h(2 + nblocks);
+    CK(cudaMemcpyAsync(h.data(), dout, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, s));
+    if (stats && c.X->stats)
+        CK(cudaMemcpyAsync(stats, c.X->stats, sizeof(unsigned long long) * xd::ST_COUNT,
+                           cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    out[0] = h[0];
+    for (int b = 0; b < nblocks; ++b) out[1 + b] = h[2 + b];
     return MCR_OK;
 }
 

@@ -93,11 +93,36 @@ void launch_phase(mcr_matrix* h, const Vecs& V, int64_t* launches) {
     ++*launches;
 }
 
+// Reference-order dots of one reduction point (plans built by xdot_prepare beforehand: no
+// allocation may happen while a graph is being captured).
 template <int W>
 void launch_seqdot(mcr_matrix* h, const Vecs& V, int64_t* launches) {
     if (!h->seqdots) return;
-    launch_pdl(k_seqdot<W>, 1, SEQ_NT, 0, h->stream, V, (int)h->n, h->st);
+    if (h->seqdots == MCR_DOTS_SERIAL) {
+        launch_pdl(k_seqdot<W>, 1, SEQ_NT, 0, h->stream, V, (int)h->n, h->st);
+    } else {
+        const auto& P = h->xdot->plan[W];
+        launch_pdl(k_xdot<W>, P.grid, xd::NT, P.smem, h->stream, xdot_args(*h->xdot, W, nullptr),
+                   h->st);
+    }
     ++*launches;
+}
+
+// Plans of the four BiCGStab reduction points: q.r at setup (q = r), q.v, {t.t, t.s}, q.r.
+int xdot_prepare(mcr_matrix* h, const Vecs& V) {
+    if (h->seqdots != MCR_DOTS_SEQUENTIAL) return MCR_OK;
+    if (!h->xdot) h->xdot = new XdotCtx();
+    XdotCtx& X = *h->xdot;
+    const int nb = h->dot_blocks;
+    TRY(xdot_smem_attr<SQ_S0>());
+    TRY(xdot_smem_attr<SQ_V>());
+    TRY(xdot_smem_attr<SQ_T>());
+    TRY(xdot_smem_attr<SQ_E>());
+    TRY(xdot_plan(X, SQ_S0, h->stream, h->device, h->n, 1, nb, V.r, V.r, nullptr, nullptr));
+    TRY(xdot_plan(X, SQ_V, h->stream, h->device, h->n, 1, nb, V.q, V.v, nullptr, nullptr));
+    TRY(xdot_plan(X, SQ_T, h->stream, h->device, h->n, 2, nb, V.t, V.t, V.t, V.s));
+    TRY(xdot_plan(X, SQ_E, h->stream, h->device, h->n, 1, nb, V.q, V.r, nullptr, nullptr));
+    return MCR_OK;
 }
 
 // ---------------------------------------------------------------- sharded exchange points
@@ -351,16 +376,20 @@ int bicgstab_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double t
     auto body = [&](int64_t* n) {
         launch_phase<PH_A>(h, V, n);               // p = r + beta (p - w v)
         launch_mv<EPI_V>(h, false, p_full, V, n);  // v = M p, q.v -> a
+        launch_seqdot<SQ_V>(h, V, n);
         launch_phase<PH_C>(h, V, n);               // s = r - a v, max|s|
         launch_mv<EPI_T>(h, false, s_full, V, n);  // t = M s, t.t, t.s -> w
+        launch_seqdot<SQ_T>(h, V, n);
         launch_phase<PH_E>(h, V, n);               // x, r updates, q.r -> beta; loop condition
+        launch_seqdot<SQ_E>(h, V, n);
     };
     // From the second BiCGStab solve of a handle the loop is the graph from the start. On the
     // first solve of a large system (the end-to-end path uploads a fresh matrix per step) the
     // graph is captured and instantiated on the host while the first host-issued batch runs on
     // the device, and takes over from the next iteration on; for small systems capture +
     // instantiation cost more than the batch hides, so they keep the host-batched loop.
-    const bool gmode = graph_mode(h) && !h->seqdots && max_it >= 1;
+    TRY(xdot_prepare(h, V));
+    const bool gmode = graph_mode(h) && h->seqdots != MCR_DOTS_SERIAL && max_it >= 1;
     const bool first = h->bicg_solves++ == 0;
     const bool use_graph = gmode && !first;
     if (use_graph && !h->gl_bicg.exec && !h->gl_bicg.failed)
@@ -396,7 +425,7 @@ int bicgstab_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double t
             CK(cudaGraphLaunch(h->gl_bicg.exec, h->stream));
             TRY(read_state(h));
             const int U = h->gl_bicg.unroll;
-            launched += 5 * ((h->h_st->it + U) / U * U);
+            launched += (h->seqdots ? 8 : 5) * ((h->h_st->it + U) / U * U);
             iters = max_it;
         } else {
             TRY(read_state(h));
@@ -434,7 +463,7 @@ int bicgstab_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double t
                 CK(cudaGraphLaunch(h->gl_bicg.exec, h->stream));
                 TRY(read_state(h));
                 const int U = h->gl_bicg.unroll;
-                launched += 5 * ((h->h_st->it - it0 + U) / U * U);
+                launched += (h->seqdots ? 8 : 5) * ((h->h_st->it - it0 + U) / U * U);
                 break;
             }
             batch = std::min(batch * 2, 32);

@@ -1,0 +1,159 @@
+// xdot_host.cuh -- launch plans and scratch of the bit-exact sequential dots (xdot.cuh).
+// Part of the single translation unit mcr.cu (after handle.h, before solve.cuh).
+#pragma once
+
+namespace {
+
+// Scratch + one plan per reduction point (SQ_S0, SQ_V, SQ_T, SQ_E, SQ_TEST).
+struct XdotCtx {
+    int grid_cap = 0, nseq_cap = 0;
+    void* blk = nullptr;
+    size_t blk_bytes = 0;
+    xd::Scratch S{};
+    struct Plan {
+        xd::Seq* d_seqs = nullptr;
+        int nseq = 0, nseq0 = 0, ndot = 1, pardots = 0, grid = 0, E = 1, nblocks = 1;
+        const double* key[4] = {nullptr, nullptr, nullptr, nullptr};
+        size_t smem = 0;
+        int64_t n = -1;
+    } plan[5];
+    std::vector<void*> seq_bufs;
+    unsigned long long* stats = nullptr;  // MCR_XDOT_STATS=1: fallback counters (diagnostics)
+};
+
+// solvers.py:159-168 _row_blocks: base + 1 rows for the first n % k blocks
+inline void row_blocks(int64_t n, int k, std::vector<int64_t>& lo, std::vector<int64_t>& hi) {
+    lo.clear();
+    hi.clear();
+    const int64_t base = n / k, extra = n % k;
+    int64_t start = 0;
+    for (int i = 0; i < k; ++i) {
+        const int64_t size = base + (i < extra ? 1 : 0);
+        lo.push_back(start);
+        hi.push_back(start + size);
+        start += size;
+    }
+}
+
+inline int sm_count(int device) {
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+    return nsm > 0 ? nsm : 148;
+}
+
+template <int W>
+int xdot_smem_attr() {
+    static int done = 0;
+    if (done) return MCR_OK;
+    CK(cudaFuncSetAttribute(k_xdot<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)xd::smem_bytes(xd::EMAX)));
+    done = 1;
+    return MCR_OK;
+}
+
+// (Re)build plan `w`: ndot dots over n elements, pairs (u0, v0) and (u1, v1), each split into
+// `nblocks` row blocks when nblocks > 1 (parallel_dot_products).
+int xdot_plan(XdotCtx& X, int w, cudaStream_t s, int device, int64_t n, int ndot, int nblocks,
+              const double* u0, const double* v0, const double* u1, const double* v1) {
+    auto& P = X.plan[w];
+    const double* key[4] = {u0, v0, u1, v1};
+    if (P.d_seqs && P.n == n && P.ndot == ndot && P.nblocks == nblocks &&
+        std::equal(key, key + 4, P.key))
+        return MCR_OK;
+    const int nb = std::max(1, nblocks);
+    std::vector<int64_t> lo, hi;
+    row_blocks(n, nb, lo, hi);
+    const int nsm = sm_count(device);
+    const int64_t total = (int64_t)ndot * n;
+    int64_t E = (total + (int64_t)xd::NT * nsm - 1) / ((int64_t)xd::NT * nsm);
+    E = std::max<int64_t>(1, std::min<int64_t>(E, xd::EMAX));
+    if (const char* env = std::getenv("MCR_XDOT_E")) E = std::max(1, std::min(xd::EMAX, std::atoi(env)));
+    E |= 1;
+    const int64_t per = (int64_t)xd::NT * E;
+    std::vector<xd::Seq> seqs;
+    int grid = 0;
+    for (int k = 0; k < ndot; ++k) {
+        for (int b = 0; b < nb; ++b) {
+            xd::Seq q{};
+            q.u = k == 0 ? u0 : u1;
+            q.v = k == 0 ? v0 : v1;
+            q.a = lo[b];
+            q.b = hi[b];
+            q.cta0 = grid;
+            q.ncta = (int)std::max<int64_t>(1, (hi[b] - lo[b] + per - 1) / per);
+            grid += q.ncta;
+            seqs.push_back(q);
+        }
+    }
+    const int nseq = (int)seqs.size();
+    if (grid > X.grid_cap || nseq > X.nseq_cap) {
+        const int gc = std::max(grid, X.grid_cap), sc = std::max(nseq, X.nseq_cap);
+        const size_t bytes = sizeof(xd::Desc) * (size_t)gc * (1 + xd::NW) +
+                             sizeof(xd::Run) * (size_t)gc * xd::NT + sizeof(double) * (size_t)gc +
+                             sizeof(int) * (size_t)gc + sizeof(double) * (size_t)sc +
+                             sizeof(unsigned) * (size_t)(3 * sc + 1) + 256;
+        if (X.blk) CK(cudaFreeAsync(X.blk, s));
+        CK(cudaMallocAsync(&X.blk, bytes, s));
+        CK(cudaMemsetAsync(X.blk, 0, bytes, s));
+        X.blk_bytes = bytes;
+        char* p = (char*)X.blk;
+        auto take = [&](size_t b) { char* r = p; p += (b + 15) & ~(size_t)15; return r; };
+        X.S.cta = (xd::Desc*)take(sizeof(xd::Desc) * (size_t)gc);
+        X.S.warp = (xd::Desc*)take(sizeof(xd::Desc) * (size_t)gc * xd::NW);
+        X.S.runs = (xd::Run*)take(sizeof(xd::Run) * (size_t)gc * xd::NT);
+        X.S.lb_val = (double*)take(sizeof(double) * (size_t)gc);
+        X.S.result = (double*)take(sizeof(double) * (size_t)sc);
+        X.S.lb_flag = (int*)take(sizeof(int) * (size_t)gc);
+        X.S.ticket = (unsigned*)take(sizeof(unsigned) * (size_t)sc);
+        X.S.done = (unsigned*)take(sizeof(unsigned) * (size_t)sc);
+        X.S.flags = (unsigned*)take(sizeof(unsigned) * (size_t)sc);
+        X.S.all_done = (unsigned*)take(sizeof(unsigned));
+        X.grid_cap = gc;
+        X.nseq_cap = sc;
+    }
+    if (!X.stats && std::getenv("MCR_XDOT_STATS")) {
+        CK(cudaMallocAsync((void**)&X.stats, sizeof(unsigned long long) * xd::ST_COUNT, s));
+        CK(cudaMemsetAsync(X.stats, 0, sizeof(unsigned long long) * xd::ST_COUNT, s));
+    }
+    X.S.stats = X.stats;
+    if (P.d_seqs) CK(cudaFreeAsync(P.d_seqs, s));
+    CK(cudaMallocAsync((void**)&P.d_seqs, sizeof(xd::Seq) * seqs.size(), s));
+    CK(cudaMemcpyAsync(P.d_seqs, seqs.data(), sizeof(xd::Seq) * seqs.size(), cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));  // the host vector dies here
+    P.nseq = nseq;
+    P.nseq0 = nb;
+    P.ndot = ndot;
+    P.pardots = nb > 1 ? 1 : 0;
+    P.nblocks = nblocks;
+    P.grid = grid;
+    P.E = (int)E;
+    P.smem = xd::smem_bytes((int)E);
+    P.n = n;
+    std::copy(key, key + 4, P.key);
+    return MCR_OK;
+}
+
+xd::Args xdot_args(const XdotCtx& X, int w, double* out) {
+    const auto& P = X.plan[w];
+    xd::Args A{};
+    A.seqs = P.d_seqs;
+    A.nseq = P.nseq;
+    A.nseq0 = P.nseq0;
+    A.ndot = P.ndot;
+    A.pardots = P.pardots;
+    A.E = P.E;
+    A.S = X.S;
+    A.out = out;
+    return A;
+}
+
+void xdot_free(XdotCtx* X, cudaStream_t s) {
+    if (!X) return;
+    for (auto& P : X->plan)
+        if (P.d_seqs) cudaFreeAsync(P.d_seqs, s);
+    if (X->blk) cudaFreeAsync(X->blk, s);
+    if (X->stats) cudaFreeAsync(X->stats, s);
+    delete X;
+}
+
+}  // namespace

@@ -1,0 +1,55 @@
+"""The reference's inner products on the GPU, stand-alone.
+
+``dot_ascending(u, v)`` is ``_dot_ascending`` (solvers.py:136-141, ``np.cumsum(u * v)[-1]``)
+and ``dot_blocks(u, v, k)`` is ``_ParOps.dot`` with ``parallel_dot_products`` (solvers.py:
+384-396: each ``_row_blocks(n, k)`` block summed left to right, the block results added in
+ascending order from 0.0), both bit for bit, computed by ``k_xdot`` (csrc/xdot.cuh) through
+the C ABI ``mcr_xdot``. The BiCGStab solvers use the same kernel inside the solve.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+
+XDOT_STATS = ("hard_threads", "warp_tables", "cta_tables", "group_fallbacks", "cta_fallbacks",
+              "warp_fallbacks", "thread_fallbacks", "serial_sums",
+              # self-checks of a MCR_XDOT_DEBUG build
+              "dbg_runs", "dbg_runs_bad", "dbg_tables", "dbg_tables_bad", "dbg_translations",
+              "dbg_translations_bad", "dbg_spare")
+
+
+def _run(u, v, nblocks: int, device: int, stats: bool):
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    if u.shape != v.shape or u.ndim != 1:
+        raise ValueError(f"dot of shapes {u.shape} and {v.shape}")
+    L = _lib.load()
+    out = np.zeros(1 + nblocks)
+    st = np.zeros(len(XDOT_STATS), dtype=np.uint64)
+    rc = L.mcr_xdot(int(device), int(u.size), u.ctypes.data, v.ctypes.data, int(nblocks),
+                    out.ctypes.data, st.ctypes.data if stats else None)
+    if rc != _lib.MCR_OK:
+        raise _lib.NativeLibraryError(f"libmcr error {rc}: {_lib.last_error()}")
+    return out, dict(zip(XDOT_STATS, (int(x) for x in st)))
+
+
+def dot_ascending(u, v, device: int = 0) -> float:
+    """np.cumsum(u * v)[-1] (0.0 when empty), bit for bit."""
+    return float(_run(u, v, 1, device, False)[0][0])
+
+
+def dot_blocks(u, v, nblocks: int, device: int = 0):
+    """(combined dot, [block dots]) of the reference's parallel_dot_products mode."""
+    out, _ = _run(u, v, nblocks, device, False)
+    return float(out[0]), [float(x) for x in out[1:]]
+
+
+def dot_stats(u, v, nblocks: int = 1, device: int = 0):
+    """(dot, fallback counters); the counters are filled when MCR_XDOT_STATS=1 was set
+    before the library was first used."""
+    out, st = _run(u, v, nblocks, device, True)
+    return float(out[0]), st
