@@ -132,8 +132,15 @@ MCR_API int mcr_set_dot_blocks(mcr_matrix* m, int nblocks);
  * (np.cumsum(u * v)[-1] of the block, 0.0 when empty). stats (may be NULL): fallback counters,
  * filled only when the library runs with MCR_XDOT_STATS=1. Replaces _dot_ascending
  * (solvers.py:136-141) and _ParOps.dot (solvers.py:384-396). */
+/* Diagnostics: the fallback counters of a handle's reference-order dots (MCR_XDOT_STATS=1
+ * runs only; zeros otherwise), `count` entries. */
+MCR_API int mcr_xdot_stats(mcr_matrix* m, uint64_t* out, int count);
+
 MCR_API int mcr_xdot(int device, int64_t n, const double* u, const double* v, int nblocks,
                      double* out, uint64_t* stats);
+/* Same, then `reps` more launches on the device-resident inputs; *ms = mean ms per launch. */
+MCR_API int mcr_xdot_bench(int device, int64_t n, const double* u, const double* v, int nblocks,
+                           int reps, double* out, double* ms, uint64_t* stats);
 
 /* Use `stream` (a cudaStream_t on the handle's device, or NULL for the handle's own stream)
  * for every later call on this handle. */

@@ -62,6 +62,24 @@ int fail(int code, const std::string& msg) {
             return fail(MCR_CUDA_ERROR, std::string(#call) + ": " + cudaGetErrorString(e_)); \
     } while (0)
 
+// First failed kernel launch of this thread since the last launch_check(): launch_pdl records it
+// (cudaLaunchKernelEx's status) so a launch failure surfaces at the next check even when the
+// launcher itself has no status to return (graph bodies, batch loops).
+thread_local cudaError_t g_launch_err = cudaSuccess;
+
+inline void note_launch(cudaError_t e) {
+    if (e != cudaSuccess && g_launch_err == cudaSuccess) g_launch_err = e;
+}
+
+inline int launch_check() {
+    cudaError_t e = g_launch_err;
+    g_launch_err = cudaSuccess;
+    const cudaError_t last = cudaGetLastError();
+    if (e == cudaSuccess) e = last;
+    if (e != cudaSuccess) return fail(MCR_CUDA_ERROR, std::string("kernel launch: ") + cudaGetErrorString(e));
+    return MCR_OK;
+}
+
 struct DeviceGuard {
     int prev = -1;
     explicit DeviceGuard(int dev) {
@@ -199,6 +217,7 @@ struct mcr_matrix {
         unsigned long long cond = 0;
         int unroll = 1;
         bool failed = false;
+        long long key = -1;  // dot mode and blocks the body was captured with
     } gl_bicg;
     int bicg_solves = 0;
     int spmv_grid = 1;

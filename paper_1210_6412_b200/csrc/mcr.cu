@@ -498,8 +498,30 @@ MCR_API int mcr_set_dot_blocks(mcr_matrix* h, int nblocks) {
     return MCR_OK;
 }
 
+MCR_API int mcr_xdot_stats(mcr_matrix* h, uint64_t* out, int count) {
+    if (!h || !out) return fail(MCR_INVALID_ARGUMENT, "NULL argument");
+    std::lock_guard<std::mutex> lk(h->mu);
+    std::memset(out, 0, sizeof(uint64_t) * (size_t)std::max(count, 0));
+    if (!h->xdot || !h->xdot->stats) return MCR_OK;
+    DeviceGuard g(h->device);
+    const int k = std::min(count, (int)xd::ST_COUNT);
+    CK(cudaMemcpyAsync(out, h->xdot->stats, sizeof(uint64_t) * (size_t)k, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return MCR_OK;
+}
+
+MCR_API int mcr_xdot_bench(int device, int64_t n, const double* u, const double* v, int nblocks,
+                           int reps, double* out, double* ms, uint64_t* stats);
+
 MCR_API int mcr_xdot(int device, int64_t n, const double* u, const double* v, int nblocks,
                      double* out, uint64_t* stats) {
+    return mcr_xdot_bench(device, n, u, v, nblocks, 0, out, nullptr, stats);
+}
+
+// Same, timed: after one launch, `reps` more launches on device-resident inputs between two
+// CUDA events; *ms = mean milliseconds per launch (diagnostics / tools/xdot_bench.py).
+MCR_API int mcr_xdot_bench(int device, int64_t n, const double* u, const double* v, int nblocks,
+                           int reps, double* out, double* ms, uint64_t* stats) {
     if (n < 0 || nblocks < 1 || !out || (n > 0 && (!u || !v)))
         return fail(MCR_INVALID_ARGUMENT, "mcr_xdot: bad arguments");
     DeviceGuard g(device);
@@ -531,6 +553,21 @@ MCR_API int mcr_xdot(int device, int64_t n, const double* u, const double* v, in
     const auto& P = c.X->plan[SQ_TEST];
     k_xdot<SQ_TEST><<<P.grid, xd::NT, P.smem, s>>>(xdot_args(*c.X, SQ_TEST, dout), nullptr);
     CK(cudaGetLastError());
+    if (reps > 0 && ms) {
+        cudaEvent_t e0, e1;
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        CK(cudaEventRecord(e0, s));
+        for (int r = 0; r < reps; ++r)
+            k_xdot<SQ_TEST><<<P.grid, xd::NT, P.smem, s>>>(xdot_args(*c.X, SQ_TEST, dout), nullptr);
+        CK(cudaEventRecord(e1, s));
+        CK(cudaEventSynchronize(e1));
+        float t = 0.f;
+        CK(cudaEventElapsedTime(&t, e0, e1));
+        *ms = t / reps;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+    }
     std::vector<double> h(2 + nblocks);
     CK(cudaMemcpyAsync(h.data(), dout, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, s));
     if (stats && c.X->stats)
@@ -558,7 +595,7 @@ MCR_API int mcr_matvec_device(mcr_matrix* h, const double* d_x, double* d_y) {
     V.y = d_y;
     int64_t launched = 0;
     launch_mv<EPI_Y>(h, false, d_x, V, &launched);
-    CK(cudaGetLastError());
+    TRY(launch_check());
     return MCR_OK;
 }
 
@@ -575,7 +612,7 @@ MCR_API int mcr_matvec(mcr_matrix* h, const double* x, double* y) {
     V.y = h->vec(V_V);
     int64_t launched = 0;
     launch_mv<EPI_Y>(h, false, h->vec(V_P), V, &launched);
-    CK(cudaGetLastError());
+    TRY(launch_check());
     CK(cudaMemcpyAsync(y, h->vec(V_V), bytes, cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
     return MCR_OK;

@@ -61,7 +61,7 @@ void launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t sm
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
-    cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+    note_launch(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
 }
 
 template <int EPI>
@@ -141,7 +141,7 @@ int exchange_point(mcr_matrix* h, double* buf, int64_t* launches) {
     if (rc) return fail(MCR_CUDA_ERROR, std::string(T.kind()) + " exchange: " + T.err);
     launch_pdl(k_finalize<W>, 1, 32, 0, h->stream, h->st, (const double*)h->recv, h->world);
     ++*launches;
-    CK(cudaGetLastError());
+    TRY(launch_check());
     return MCR_OK;
 }
 
@@ -166,7 +166,7 @@ int p2p_barrier(mcr_matrix* h) {
 int residual_into_state(mcr_matrix* h, const double* x, int64_t* launches) {
     Vecs V = base_vecs(h);
     launch_mv<EPI_RESID>(h, false, x, V, launches);
-    CK(cudaGetLastError());
+    TRY(launch_check());
     if (h->sharded()) TRY(exchange_point<FIN_RESID>(h, nullptr, launches));
     return MCR_OK;
 }
@@ -252,6 +252,7 @@ constexpr int GRAPH_UNROLL_BICG = 4;    // iterations per while-body (1: 10.51, 
 // Any failure to build it leaves the host-batched loop in use.
 template <class Body>
 int build_graph_loop(mcr_matrix* h, mcr_matrix::GraphLoop& G, int unroll, Body body) {
+    TRY(launch_check());  // errors from before the capture are the caller's, not the capture's
     cudaGraph_t g = nullptr;
     cudaStream_t cs = nullptr;
     cudaStream_t saved = h->stream;
@@ -281,7 +282,8 @@ int build_graph_loop(mcr_matrix* h, mcr_matrix::GraphLoop& G, int unroll, Body b
     cudaGraphExec_t exec = nullptr;
     ok = ok && cudaGraphInstantiate(&exec, g, 0) == cudaSuccess;
     if (cs) cudaStreamDestroy(cs);
-    cudaGetLastError();  // a failed attempt must not leave a sticky error for the next call
+    g_launch_err = cudaSuccess;  // a failed capture attempt must not leave an error behind
+    cudaGetLastError();
     if (!ok) {
         if (g) cudaGraphDestroy(g);
         G.failed = true;
@@ -337,7 +339,7 @@ int jacobi_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double tol
                 TRY(exchange_point<FIN_JACOBI>(h, h->p2p ? nullptr : wrote, &launched));
             }
         }
-        CK(cudaGetLastError());
+        TRY(launch_check());
         sweeps += k;
         TRY(read_state(h));
         if (h->h_st->stop || sweeps >= max_it) break;
@@ -389,6 +391,14 @@ int bicgstab_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double t
     // the device, and takes over from the next iteration on; for small systems capture +
     // instantiation cost more than the batch hides, so they keep the host-batched loop.
     TRY(xdot_prepare(h, V));
+    // the captured body depends on the dot mode (and the block plan): rebuild when it changed
+    const long long gkey = (long long)h->seqdots * 1000003ll + h->dot_blocks;
+    if (h->gl_bicg.key != gkey) {
+        if (h->gl_bicg.exec) cudaGraphExecDestroy(h->gl_bicg.exec);
+        if (h->gl_bicg.graph) cudaGraphDestroy(h->gl_bicg.graph);
+        h->gl_bicg = mcr_matrix::GraphLoop{};
+        h->gl_bicg.key = gkey;
+    }
     const bool gmode = graph_mode(h) && h->seqdots != MCR_DOTS_SERIAL && max_it >= 1;
     const bool first = h->bicg_solves++ == 0;
     const bool use_graph = gmode && !first;
@@ -419,7 +429,7 @@ int bicgstab_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double t
         // r = b - 1.0 * M x0, q = r, p = v = 0
         launch_mv<EPI_S0>(h, false, h->vec(V_X), V, &launched);
         launch_seqdot<SQ_S0>(h, V, &launched);
-        CK(cudaGetLastError());
+        TRY(launch_check());
         if (sh) TRY(exchange_point<FIN_S0>(h, nullptr, &launched));
         if (graph) {  // the loop runs on the device; a solve stopped by S0 ends after one body
             CK(cudaGraphLaunch(h->gl_bicg.exec, h->stream));
@@ -449,7 +459,7 @@ int bicgstab_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double t
             launch_seqdot<SQ_E>(h, V, &launched);
             if (sh) TRY(exchange_point<FIN_E>(h, nullptr, &launched));
         }
-        CK(cudaGetLastError());
+        TRY(launch_check());
         iters += k;
         if (late_graph) {  // host work while the batch runs
             late_graph = false;

@@ -10,34 +10,35 @@
 //   multiple of u and a step is a TRANSLATION: fl(s + p) = s + D(p, parity of s/u), where
 //   the parity only matters for exact ties (round half to even). So a stretch of elements
 //   whose partial sums stay inside one binade (a "run") is summarised by two displacements
-//   d0 / d1 (start index even / odd) and an excursion bound x: for ANY start s in that
-//   binade with |s| - x and |s| + x still inside it, the stretch ends at s + d[parity(s)].
-//   Two runs of the same binade compose associatively. d0, d1 come from summing the stretch
-//   from two reference starts in the middle of the binade (plain DADD chains, exact).
+//   d[0] / d[1] (start index even / odd) and the range [lo, hi] its partial sums move through:
+//   for ANY start s in that binade with s + [lo, hi] one ulp clear of the binade's ends, the
+//   stretch ends at s + d[parity(s)]. Runs of one binade compose associatively. d, lo, hi
+//   come from summing the stretch from two reference starts in the middle of the binade.
 // * Where the sum changes binade (crossings, passes near zero) a "table" describes the
 //   stretch as a function of its start: 32 consecutive candidate starts (doubles around a
 //   predicted start) are carried through the stretch exactly (runs applied per candidate,
 //   anything else added element by element), and each candidate keeps the range [lo, hi] of
-//   start shifts delta that leave every partial sum inside its binade with one ulp of margin
-//   plus the coarsest grid 2^km it passed. A start s = cand_k + delta in cand_k's binade
-//   with delta in [lo, hi] and delta = 0 mod 2^km (k = the candidate congruent to s mod 32
-//   ulps) ends at out_k + delta: every rounding step commutes with such a shift.
-// * Tables compose (evaluate the second at the first's outputs) — that is how warps, CTAs
-//   and the whole vector are stitched together. Predicted starts come from a plain
-//   (non-exact) prefix sum of the products; a prediction only has to land in the right
-//   binade for runs and within the translation range for tables. Nothing is ever assumed:
-//   every use of a run or table is checked, and a failed check falls back to the finer
-//   level (CTA -> warp pieces -> thread pieces -> element-by-element), so the result is the
-//   reference's bits for every input (NaN/Inf/overflow/-0.0 included); only the time
-//   depends on how often a fallback is needed.
+//   start shifts delta that leave every partial sum inside its binade one ulp clear of its
+//   ends, plus the coarsest grid 2^km it passed. A start s = cand_k + delta in cand_k's
+//   binade with delta in [lo, hi] and delta = 0 mod 2^km (k = the candidate congruent to s
+//   mod 32 ulps) ends at out_k + delta: every rounding step commutes with such a shift.
+// * Tables compose (evaluate the second at the first's outputs): that is how warps and CTAs
+//   are stitched together. Predicted starts come from a plain (non-exact) prefix sum of the
+//   products; a prediction only has to land in the right binade for runs and within the
+//   translation range for tables. Nothing is assumed: every use of a run or table is
+//   checked, and where a check fails the stretch is recomputed from the exact start (a CTA's
+//   range rebuilt with its true start; a thread's elements added one by one), so the result
+//   is the reference's bits for every input (NaN / Inf / overflow / -0.0 included); only the
+//   time depends on how often that happens.
 //
 // One launch per reduction point: a CTA owns NT*E consecutive elements of one sequence
 // (thread t owns E consecutive ones, E odd so the shared-memory reads are conflict free),
-// builds thread runs -> warp pieces -> a CTA piece, publishes it; the last CTA of the
-// sequence composes the CTA pieces (8 warps on 8 consecutive groups, then a scalar walk of
-// the true value from 0.0) and runs the BiCGStab scalar step. Sequences: one per dot, or one
-// per row block when the reference's parallel_dot_products mode is on (solvers.py:384-396:
-// each block summed sequentially, block results added in ascending order from 0.0).
+// builds thread runs -> warp pieces -> a CTA piece and publishes it; the last CTA of the
+// sequence stages the CTA pieces in shared memory, composes 7 groups of them (warps 1..7)
+// while warp 0 carries the true value from 0.0 through group 0, then through the group
+// tables, and runs the BiCGStab scalar step. Sequences: one per dot, or one per row block
+// when the reference's parallel_dot_products mode is on (solvers.py:384-396: each block
+// summed sequentially, block results added in ascending order from 0.0).
 #pragma once
 
 #include "common.cuh"
@@ -45,9 +46,9 @@
 namespace mcr {
 namespace xd {
 
-constexpr int NT = 256;
+constexpr int NT = 512;
 constexpr int NW = NT / 32;
-constexpr int EMAX = 63;
+constexpr int EMAX = 31;
 constexpr unsigned long long MANT = 0x000FFFFFFFFFFFFFull;
 constexpr unsigned long long SGN = 0x8000000000000000ull;
 constexpr int KM_NONE = -4096;
@@ -60,27 +61,45 @@ enum Stat : int { ST_HARD = 0, ST_WARP_TABLE, ST_CTA_TABLE, ST_GROUP_FB, ST_CTA_
                   ST_CHUNK_FB, ST_SERIAL,
                   // MCR_XDOT_DEBUG builds: self-checks of every piece against element-by-element sums
                   ST_DBG_RUN, ST_DBG_RUN_BAD, ST_DBG_TAB, ST_DBG_TAB_BAD, ST_DBG_TR, ST_DBG_TR_BAD,
-                  ST_DBG_LEVEL_BAD, ST_COUNT };
+                  ST_DBG_SPARE,
+                  // why the true value could not use a piece (debug builds)
+                  ST_R_HOLE, ST_R_SIGN, ST_R_EXP, ST_R_SLACK, ST_R_KM, ST_R_RUN_BIN, ST_R_RUN_BOUND,
+                  // MCR_XDOT_TIMING builds: SM cycles per phase (CTA phases summed over CTAs)
+                  ST_T_LOAD, ST_T_LOOKBACK, ST_T_RUNS, ST_T_CTA, ST_T_ROOT_GROUPS, ST_T_ROOT_WALK,
+                  ST_T_LAUNCHES,
+                  // MCR_XDOT_TIMING: ns per launch (globaltimer): entry skew, entry -> last build end,
+                  // last build end -> root start... root end, and min-entry -> root end
+                  ST_G_SKEW, ST_G_BUILD, ST_G_ROOT, ST_G_TOTAL, ST_G_MIN_ENTRY, ST_G_MAX_ENTRY,
+                  ST_G_MAX_BUILD,
+                  // per-launch max of the CTA phases (slots), summed over launches
+                  ST_M_LOAD, ST_M_LOOKBACK, ST_M_RUNS, ST_M_CTA, ST_MS_LOAD, ST_MS_LOOKBACK, ST_MS_RUNS,
+                  ST_MS_CTA, ST_SIMS_WARP, ST_SIMS_CTA,
+                  ST_W_CHAIN, ST_W_MERGE, ST_W_TABLE, ST_WS_CHAIN, ST_WS_MERGE, ST_WS_TABLE,
+                  ST_W_SLOWEST, ST_COUNT };
 
-struct Run {        // 32 B
-    double d0, d1;  // displacement for a start of even / odd index
-    double x;       // excursion bound
+struct Run {        // 56 B
+    double d[2];    // displacement for a start of even / odd index
+    double lo[2], hi[2];  // range of the partial sums' displacement from the start (per start parity)
     int e, neg;     // binade; e = E_HARD (not a run) or E_EMPTY (identity)
 };
-struct Lane {       // 32 B: one candidate of a table
+struct LaneR {      // one candidate of a table, as carried in registers
     double out, lo, hi;
     int km, hole;
 };
-struct Hdr {        // 64 B
+struct LaneS {      // ... and as stored: slack bounds rounded inwards to float (conservative)
+    double out;
+    float lo, hi;
+};
+struct Hdr {        // 80 B
     int kind, neg, e, pad;
     unsigned long long mb0;  // table: magnitude bits of candidate 0
-    double d0, d1, x;        // run
     double pred;             // predicted start of the piece (window of later tables)
-    double pad2;
+    double d[2], lo[2], hi[2];  // run
 };
-struct Desc {       // 1088 B
+struct Desc {       // 720 B
     Hdr h;
-    Lane l[32];
+    LaneS l[32];
+    int kmh[32];    // km << 1 | hole
 };
 
 // One sequence: sum_{i=a}^{b-1} u[i] v[i] in index order. CTAs [cta0, cta0 + ncta).
@@ -93,9 +112,7 @@ struct Seq {
 
 // Scratch (device memory owned by the plan).
 struct Scratch {
-    Desc* cta;             // [grid]
-    Desc* warp;            // [grid * NW]
-    Run* runs;             // [grid * NT]
+    Desc* cta;             // [grid] the CTA pieces
     double* lb_val;        // [grid] look-back: CTA totals (predictions only)
     int* lb_flag;          // [grid]
     unsigned* ticket;      // [nseq]
@@ -113,6 +130,8 @@ struct Args {
     int ndot;       // 1 or 2
     int pardots;    // combine the sequences of a dot as the reference's block partials
     int E;
+    int stage;      // CTA pieces the root stages in shared memory at a time
+    int upto;       // diagnostics (MCR_XDOT_UPTO): stop after build phase 1..4 (0 = complete)
     Scratch S;
     double* out;    // test mode: the dot results go here (no solver state)
 };
@@ -123,6 +142,18 @@ __device__ __forceinline__ int dexp(unsigned long long b) { return (int)((b >> 5
 __device__ __forceinline__ void stat(const Scratch& S, int k) {
     if (S.stats) atomicAdd(S.stats + k, 1ull);
 }
+#ifdef MCR_XDOT_TIMING
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define XT_MARK(t) long long t = (long long)gtime()
+#define XT_ADD(S, k, t0) do { if ((S).stats && threadIdx.x == 0) { const unsigned long long d_ = (unsigned long long)((long long)gtime() - (t0)); atomicAdd((S).stats + (k), d_); if ((k) >= ST_T_LOAD && (k) <= ST_T_CTA) atomicMax((S).stats + ST_M_LOAD + ((k) - ST_T_LOAD), d_); } } while (0)
+#else
+#define XT_MARK(t) do {} while (0)
+#define XT_ADD(S, k, t0) do {} while (0)
+#endif
 
 // parity of D/u for a displacement D that is a multiple of u = ulp(binade e) (e >= RUN_MIN_E,
 // so a non-zero D is a normal number): the bit of D's significand that has weight u
@@ -133,37 +164,60 @@ __device__ __forceinline__ int disp_parity(double D, int e) {
     return (int)((((b & MANT) | (1ull << 52)) >> sh) & 1ull);
 }
 
-// a then b (same binade, or either empty)
+__device__ __forceinline__ Run run_empty() {
+    Run r;
+    r.d[0] = r.d[1] = r.lo[0] = r.lo[1] = r.hi[0] = r.hi[1] = 0.0;
+    r.e = E_EMPTY;
+    r.neg = 0;
+    return r;
+}
+
+// a then b (same binade, or either empty). All quantities are multiples of u smaller than the
+// binade: the sums are exact. (Selects, not b.d[m]: a runtime index would put the structs in
+// local memory.)
 __device__ __forceinline__ Run run_merge(const Run& a, const Run& b) {
     if (a.e == E_EMPTY) return b;
     if (b.e == E_EMPTY) return a;
     Run r;
     r.e = a.e;
     r.neg = a.neg;
-    r.d0 = dadd(a.d0, disp_parity(a.d0, a.e) ? b.d1 : b.d0);        // start index even
-    r.d1 = dadd(a.d1, (1 ^ disp_parity(a.d1, a.e)) ? b.d1 : b.d0);  // start index odd
-    r.x = __dadd_ru(a.x, b.x);
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+        const bool m = (p ^ disp_parity(a.d[p], a.e)) != 0;  // parity of the index after a
+        const double bd = m ? b.d[1] : b.d[0], bl = m ? b.lo[1] : b.lo[0], bh = m ? b.hi[1] : b.hi[0];
+        r.d[p] = dadd(a.d[p], bd);
+        r.lo[p] = fmin(a.lo[p], dadd(a.d[p], bl));
+        r.hi[p] = fmax(a.hi[p], dadd(a.d[p], bh));
+    }
     return r;
 }
 
-// Does the run R apply to a start v? If so v advances and the start-shift constraints of the
-// carried piece (lo, hi, km) tighten.
+// Does the run R apply to a start v? It does when v is in R's binade and every partial sum
+// v + [lo, hi] stays one ulp clear of the binade's ends; then v advances and the start-shift
+// constraints of the carried piece (lo, hi, km) tighten.
 __device__ __forceinline__ bool run_apply(const Run& R, double& v, double& lo, double& hi, int& km) {
     if (R.e == E_EMPTY) return true;
     const unsigned long long b = bt(v);
     const int ng = (int)(b >> 63);
     if (R.e == E_HARD || dexp(b) != R.e || ng != R.neg) return false;
-    const double lowlim = __dadd_ru(fb(((unsigned long long)R.e << 52) | 1ull), R.x);     // 2^e + u + x
-    const double highlim = __dsub_rd(fb(((unsigned long long)R.e << 52) | MANT), R.x);    // 2^(e+1) - u - x
-    const double av = fabs(v);
-    if (!(av >= lowlim && av <= highlim)) return false;
+    const bool odd = (b & 1ull) != 0;
+    const double bot = fb(((unsigned long long)ng << 63) | ((unsigned long long)R.e << 52) | 1ull);  // +-(2^e + u)
+    const double top = fb(((unsigned long long)ng << 63) | ((unsigned long long)R.e << 52) | MANT); // +-(2^(e+1) - u)
+    const double vlo = dadd(v, odd ? R.lo[1] : R.lo[0]), vhi = dadd(v, odd ? R.hi[1] : R.hi[0]);  // exact
     double a, c;
-    if (!ng) { a = __dsub_ru(lowlim, v); c = __dsub_rd(highlim, v); }
-    else { a = __dsub_ru(-highlim, v); c = __dsub_rd(-lowlim, v); }
+    if (!ng) {
+        if (!(vlo >= bot && vhi <= top)) return false;
+        a = dsub(bot, vlo);
+        c = dsub(top, vhi);
+    } else {
+        if (!(vhi <= bot && vlo >= top)) return false;
+        a = dsub(top, vlo);
+        c = dsub(bot, vhi);
+    }
     lo = fmax(lo, a);
     hi = fmin(hi, c);
     km = max(km, R.e - 1074);
-    v = dadd(v, (b & 1ull) ? R.d1 : R.d0);  // exact: stays on the grid of the binade
+    v = dadd(v, odd ? R.d[1] : R.d[0]);  // exact: stays on the grid of the binade
     return true;
 }
 
@@ -190,7 +244,7 @@ __device__ __forceinline__ void sim_step(double& v, double p, double& lo, double
 
 // Warp-collective: evaluate the table (this lane holds entry `lane`; mb0/tneg uniform) at
 // this lane's s. On success out = the table's value at s and lo/hi/km tighten.
-__device__ __forceinline__ bool table_eval(unsigned long long mb0, int tneg, const Lane& T, double s,
+__device__ __forceinline__ bool table_eval(unsigned long long mb0, int tneg, const LaneR& T, double s,
                                            double& out, double& lo, double& hi, int& km) {
     const unsigned long long b = bt(s);
     const unsigned long long mb = b & ~SGN;
@@ -220,15 +274,6 @@ __device__ __forceinline__ bool table_eval(unsigned long long mb0, int tneg, con
     return true;
 }
 
-// Same for a uniform scalar s (every lane gets the result).
-__device__ __forceinline__ bool table_eval_scalar(unsigned long long mb0, int tneg, const Lane& T, double& s) {
-    double lo = -INFINITY, hi = INFINITY, out = 0.0;
-    int km = KM_NONE;
-    const bool ok = table_eval(mb0, tneg, T, s, out, lo, hi, km);
-    if (ok) s = out;
-    return ok;
-}
-
 __device__ __forceinline__ unsigned long long window_mb0(double pred) {
     const unsigned long long mb = bt(pred) & ~SGN;
     unsigned long long m0 = mb > 16 ? mb - 16 : 0;
@@ -243,69 +288,139 @@ __device__ __forceinline__ double cand(unsigned long long mb0, int neg, int j) {
 
 __device__ __forceinline__ Run hdr_run(const Hdr& h) {
     Run r;
-    r.d0 = h.d0; r.d1 = h.d1; r.x = h.x; r.e = h.e; r.neg = h.neg;
+    r.d[0] = h.d[0]; r.d[1] = h.d[1]; r.lo[0] = h.lo[0]; r.lo[1] = h.lo[1];
+    r.hi[0] = h.hi[0]; r.hi[1] = h.hi[1]; r.e = h.e; r.neg = h.neg;
     return r;
 }
 __device__ __forceinline__ void hdr_set_run(Hdr& h, const Run& r, double pred) {
-    h.kind = K_RUN; h.e = r.e; h.neg = r.neg; h.d0 = r.d0; h.d1 = r.d1; h.x = r.x;
-    h.pred = pred; h.mb0 = 0; h.pad = 0; h.pad2 = 0.0;
+    h.kind = K_RUN; h.e = r.e; h.neg = r.neg; h.pad = 0; h.mb0 = 0; h.pred = pred;
+    h.d[0] = r.d[0]; h.d[1] = r.d[1]; h.lo[0] = r.lo[0]; h.lo[1] = r.lo[1];
+    h.hi[0] = r.hi[0]; h.hi[1] = r.hi[1];
+}
+__device__ __forceinline__ void hdr_set_table(Hdr& h, unsigned long long mb0, int neg, double pred) {
+    h.kind = K_TABLE; h.e = 0; h.neg = neg; h.pad = 0; h.mb0 = mb0; h.pred = pred;
+    h.d[0] = h.d[1] = h.lo[0] = h.lo[1] = h.hi[0] = h.hi[1] = 0.0;
 }
 __device__ __forceinline__ bool runs_compatible(const Run& a, const Run& b) {
     return a.e == E_EMPTY || b.e == E_EMPTY || (a.e != E_HARD && a.e == b.e && a.neg == b.neg);
 }
+__device__ __forceinline__ void store_lane(Desc* D, int lane, const LaneR& L) {
+    LaneS s;
+    s.out = L.out;
+    s.lo = __double2float_ru(L.lo);  // inwards: a smaller shift range is still a valid one
+    s.hi = __double2float_rd(L.hi);
+    D->l[lane] = s;
+    D->kmh[lane] = (L.km << 1) | (L.hole ? 1 : 0);
+}
+__device__ __forceinline__ LaneR load_lane(const Desc* D, int lane) {
+    const LaneS s = D->l[lane];
+    const int kmh = D->kmh[lane];
+    LaneR L;
+    L.out = s.out;
+    L.lo = (double)s.lo;
+    L.hi = (double)s.hi;
+    L.km = kmh >> 1;
+    L.hole = kmh & 1;
+    return L;
+}
 
-// Warp-collective: carry this lane's value (lo/hi/km) through one piece (run or table).
-// A table piece's entries are read from `D` (shared or global memory).
-__device__ __forceinline__ bool piece_apply(const Desc* D, double& v, double& lo, double& hi, int& km) {
-    const int lane = threadIdx.x & 31;
-    const int kind = D->h.kind;
-    if (kind == K_RUN) {
-        const Run R = hdr_run(D->h);
-        return run_apply(R, v, lo, hi, km);
-    }
-    const Lane T = D->l[lane];
-    value_slack(v, lo, hi, km);
-    double out;
-    const bool ok = table_eval(D->h.mb0, D->h.neg, T, v, out, lo, hi, km);
-    if (ok) v = out;
+// A piece as a warp holds it: the uniform header plus this lane's table entry.
+struct PieceR {
+    int kind, neg;
+    unsigned long long mb0;
+    Run R;
+    LaneR T;
+};
+__device__ __forceinline__ PieceR load_piece(const Desc* D) {
+    PieceR P;
+    const Hdr h = D->h;
+    P.kind = h.kind;
+    P.neg = h.neg;
+    P.mb0 = h.mb0;
+    P.R = hdr_run(h);
+    P.T = load_lane(D, threadIdx.x & 31);
+    return P;
+}
+// Warp-collective for tables (kind is the same in every lane: the branch does not diverge):
+// carry this lane's value through the piece.
+__device__ __forceinline__ bool piece_apply_r(const PieceR& P, double& v, double& lo, double& hi, int& km) {
+    if (P.kind == K_RUN) return run_apply(P.R, v, lo, hi, km);
+    double out = 0.0, l2 = lo, h2 = hi;
+    int k2 = km;
+    value_slack(v, l2, h2, k2);
+    const bool ok = table_eval(P.mb0, P.neg, P.T, v, out, l2, h2, k2);
+    if (ok) { v = out; lo = l2; hi = h2; km = k2; }
     return ok;
 }
 
-// ---------------------------------------------------------------- scalar walks (fallbacks)
-// Uniform across the warp: every lane carries the same value.
-__device__ bool piece_scalar(const Desc* D, double& v) {
-    if (D->h.kind == K_RUN) {
-        double lo = -INFINITY, hi = INFINITY;
-        int km = KM_NONE;
-        return run_apply(hdr_run(D->h), v, lo, hi, km);
+// Elements added one by one, carrying the start-shift constraints of every partial sum: the
+// add chain plus, per stretch of one binade, the min / max of the partial sums' bit patterns
+// (for one sign they order like the magnitudes); at a change of binade (sign and exponent
+// bits) the stretch's constraints are those of its two extremes.
+__device__ __forceinline__ void flush_range(unsigned long long bmin, unsigned long long bmax, double& lo,
+                                            double& hi, int& km) {
+    value_slack(fb(bmin), lo, hi, km);
+    value_slack(fb(bmax), lo, hi, km);
+}
+__device__ __forceinline__ void sim_elems_slow(const double* p, int cnt, double& v, double& lo, double& hi, int& km) {
+    if (cnt <= 0) return;
+    double x = dadd(v, p[0]);
+    unsigned long long bmin = bt(x), bmax = bmin, top = bmin >> 52;
+    for (int k = 1; k < cnt; ++k) {
+        x = dadd(x, p[k]);
+        const unsigned long long b = bt(x);
+        if ((b >> 52) != top) {
+            flush_range(bmin, bmax, lo, hi, km);
+            bmin = bmax = b;
+            top = b >> 52;
+        } else {
+            bmin = min(bmin, b);
+            bmax = max(bmax, b);
+        }
     }
-    const Lane T = D->l[threadIdx.x & 31];
-    return table_eval_scalar(D->h.mb0, D->h.neg, T, v);
+    flush_range(bmin, bmax, lo, hi, km);
+    v = x;
+}
+// Branch-free common case: the partial sums fall into at most two binades (the first one's and
+// one other); the extremes are kept per binade. Anything else: the per-stretch path above.
+__device__ __forceinline__ void sim_elems(const double* p, int cnt, double& v, double& lo, double& hi, int& km) {
+    if (cnt <= 0) return;
+    double x = dadd(v, p[0]);
+    const unsigned long long t0 = bt(x) >> 52;
+    unsigned long long amin = bt(x), amax = amin, bmin = ~0ull, bmax = 0ull;
+#pragma unroll 4
+    for (int k = 1; k < cnt; ++k) {
+        x = dadd(x, p[k]);
+        const unsigned long long b = bt(x);
+        const bool inA = (b >> 52) == t0;
+        amin = inA ? min(amin, b) : amin;
+        amax = inA ? max(amax, b) : amax;
+        bmin = inA ? bmin : min(bmin, b);
+        bmax = inA ? bmax : max(bmax, b);
+    }
+    if (bmax != 0ull && (bmin >> 52) != (bmax >> 52)) {  // a third binade: redo per stretch
+        sim_elems_slow(p, cnt, v, lo, hi, km);
+        return;
+    }
+    flush_range(amin, amax, lo, hi, km);
+    if (bmax != 0ull) flush_range(bmin, bmax, lo, hi, km);
+    v = x;
 }
 
-__device__ void walk_chunk(const Args& A, const Seq& q, int slot, int ci, int t, double& v) {
-    const Run R = A.S.runs[(size_t)slot * NT + t];
-    double lo = -INFINITY, hi = INFINITY;
-    int km = KM_NONE;
-    if (R.e == E_EMPTY || run_apply(R, v, lo, hi, km)) return;
-    stat(A.S, ST_CHUNK_FB);
-    const long long c0 = q.a + (long long)ci * NT * A.E;
-    const long long i0 = c0 + (long long)t * A.E;
-    const long long i1 = min(min(q.b, c0 + (long long)NT * A.E), i0 + A.E);
-    for (long long i = i0; i < i1; ++i) v = dadd(v, dmul(__ldcg(q.u + i), __ldcg(q.v + i)));
-}
-
-__device__ void walk_warp(const Args& A, const Seq& q, int slot, int ci, int w, double& v) {
-    if (piece_scalar(A.S.warp + (size_t)slot * NW + w, v)) return;
-    stat(A.S, ST_WARP_FB);
-    for (int c = 0; c < 32; ++c) walk_chunk(A, q, slot, ci, w * 32 + c, v);
-}
-
-__device__ void walk_cta(const Args& A, const Seq& q, int ci, double& v) {
-    const int slot = q.cta0 + ci;
-    if (piece_scalar(A.S.cta + slot, v)) return;
-    stat(A.S, ST_CTA_FB);
-    for (int w = 0; w < NW; ++w) walk_warp(A, q, slot, ci, w, v);
+// Per lane, no collectives: carry v through the thread runs [t0, t1) of the CTA range in shared
+// memory, adding a thread's products one by one where its run does not apply.
+__device__ void lane_walk_threads(const Run* s_runs, const double* sp, int len, int E, int t0, int t1,
+                                  double& v, double& lo, double& hi, int& km,
+                                  unsigned long long* sims = nullptr) {
+    for (int t = t0; t < t1; ++t) {
+        const Run R = s_runs[t];
+        if (run_apply(R, v, lo, hi, km)) continue;
+        const int b0 = t * E, bl = max(0, min(E, len - b0));
+#ifdef MCR_XDOT_TIMING
+        if (sims) atomicAdd(sims, 1ull);
+#endif
+        sim_elems(sp + b0, bl, v, lo, hi, km);
+    }
 }
 
 #ifdef MCR_XDOT_DEBUG
@@ -314,9 +429,9 @@ __device__ double dbg_serial(const Seq& q, long long i0, long long i1, double v)
     return v;
 }
 __device__ __forceinline__ bool same_bits(double a, double b) { return bt(a) == bt(b); }
-// this lane's table entry (start cand) over elements [i0, i1): exact value, and one translation
+// this lane's table entry (start c) over elements [i0, i1): exact value, and one translation
 __device__ void dbg_check_lane(const Scratch& S, const Seq& q, long long i0, long long i1, double c,
-                               const Lane& Lx, int level) {
+                               const LaneR& Lx, int level) {
     if (Lx.hole) return;
     const double want = dbg_serial(q, i0, i1, c);
     stat(S, ST_DBG_TAB);
@@ -342,50 +457,95 @@ __device__ void dbg_check_lane(const Scratch& S, const Seq& q, long long i0, lon
         }
     }
 }
+__device__ void why_failed(const Scratch& S, const Desc* D, double v) {
+    if ((threadIdx.x & 31) != 0 || !S.stats) return;
+    const unsigned long long b = bt(v);
+    if (D->h.kind == K_RUN) {
+        const Run R = hdr_run(D->h);
+        if (R.e == E_HARD || dexp(b) != R.e || (int)(b >> 63) != R.neg) stat(S, ST_R_RUN_BIN);
+        else stat(S, ST_R_RUN_BOUND);
+        return;
+    }
+    const unsigned long long mb = b & ~SGN, mb0 = D->h.mb0;
+    const long long d = (long long)(mb - mb0);
+    const int k = (int)(d & 31);
+    const LaneR T = load_lane(D, k);
+    if (T.hole) { stat(S, ST_R_HOLE); return; }
+    if ((int)(b >> 63) != D->h.neg) { stat(S, ST_R_SIGN); return; }
+    const unsigned long long cb = mb0 + (unsigned long long)k;
+    if (dexp(cb) != dexp(mb) || dexp(mb) == 0 || dexp(mb) == 0x7ff) { stat(S, ST_R_EXP); return; }
+    const double dl = dsub(v, fb(cb | ((unsigned long long)D->h.neg << 63)));
+    if (!(dl >= T.lo && dl <= T.hi)) { stat(S, ST_R_SLACK); return; }
+    stat(S, ST_R_KM);
+}
 #endif
 
-// ---------------------------------------------------------------- the kernel pieces
-// Phase 1-3 of a CTA: products -> thread runs -> warp pieces -> CTA piece (published).
-// Returns the CTA's local index (its ticket) in the sequence.
-__device__ int build_cta(const Args& A, const Seq& q, int si, double* sp, Run* s_runs, Desc* s_wd,
-                         double* s_red) {
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const Scratch& S = A.S;
-    const int E = A.E;
-    __shared__ int s_tk;
+// ---------------------------------------------------------------- one CTA range
+// Shared memory of a CTA (dynamic): the range's products, its thread runs, its warp pieces,
+// the root's group tables, and the root's staging area for CTA pieces.
+struct Smem {
+    double* sp;     // NT * E
+    Run* runs;      // NT
+    Desc* wd;       // NW: warp pieces (then the CTA tree)
+    Desc* gd;       // NW: the root's group tables
+    Desc* td;       // NW: the root's tree over the group tables
+    Desc* stage;    // A.stage
+};
+__host__ __device__ constexpr size_t smem_bytes(int E, int stage) {
+    return sizeof(double) * (size_t)NT * (size_t)E + sizeof(Run) * NT + sizeof(Desc) * (3 * NW + stage);
+}
+__device__ __forceinline__ Smem smem_layout(unsigned char* base, int E) {
+    Smem M;
+    M.sp = (double*)base;
+    M.runs = (Run*)(base + sizeof(double) * (size_t)NT * (size_t)E);
+    M.wd = (Desc*)(M.runs + NT);
+    M.gd = M.wd + NW;
+    M.td = M.gd + NW;
+    M.stage = M.td + NW;
+    return M;
+}
+
+// All threads: products of elements [c0, c0 + len) into sp (32 loads in flight per thread);
+// returns the CTA-wide OR of the flags (bit 0 a product that is not -0.0, bit 1 non-finite).
+__device__ unsigned load_products(const Seq& q, long long c0, int len, double* sp) {
     __shared__ unsigned s_fl;
-    __shared__ double s_pred;
-    if (tid == 0) {
-        s_tk = (int)atomicAdd(S.ticket + si, 1u);
-        s_fl = 0u;
-    }
+    if (threadIdx.x == 0) s_fl = 0u;
     __syncthreads();
-    const int ci = s_tk;
-    const int slot = q.cta0 + ci;
-    const long long c0 = q.a + (long long)ci * NT * E;
-    const long long c1 = min(q.b, c0 + (long long)NT * E);
-    const int len = (int)max(0ll, c1 - c0);
-    // products, coalesced, into shared memory
     unsigned fl = 0u;
-    for (int k = tid; k < len; k += NT) {
-        const double p = dmul(__ldcg(q.u + c0 + k), __ldcg(q.v + c0 + k));
-        const unsigned long long pb = bt(p);
-        fl |= (pb != SGN) ? 1u : 0u;
-        fl |= (dexp(pb) == 0x7ff) ? 2u : 0u;
-        sp[k] = p;
+    for (int k0 = threadIdx.x; k0 < len; k0 += NT * 16) {
+        double a[16], b[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const int k = k0 + j * NT;
+            a[j] = k < len ? __ldcg(q.u + c0 + k) : 0.0;
+            b[j] = k < len ? __ldcg(q.v + c0 + k) : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const int k = k0 + j * NT;
+            if (k < len) {
+                const double p = dmul(a[j], b[j]);
+                const unsigned long long pb = bt(p);
+                fl |= (pb != SGN) ? 1u : 0u;
+                fl |= (dexp(pb) == 0x7ff) ? 2u : 0u;
+                sp[k] = p;
+            }
+        }
     }
     if (fl) atomicOr(&s_fl, fl);
     __syncthreads();
-    // pass 1 over this thread's elements: plain sum (prediction) and sum of |p|
+    return s_fl;
+}
+
+// All threads: plain sum of this thread's E products, block exclusive scan. Returns this
+// thread's exclusive prefix; *total = the CTA's sum (same in every thread).
+__device__ double thread_scan(const double* sp, int len, int E, double* s_red, double* total) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int t0 = tid * E;
     const int tl = max(0, min(E, len - t0));
-    double ts = 0.0, ta = 0.0;
-    for (int k = 0; k < tl; ++k) {
-        const double p = sp[t0 + k];
-        ts = dadd(ts, p);
-        ta = __dadd_ru(ta, fabs(p));
-    }
-    // block exclusive scan of ts
+    double ts = 0.0;
+#pragma unroll 4
+    for (int k = 0; k < tl; ++k) ts = dadd(ts, sp[t0 + k]);
     double inc = ts;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
@@ -394,19 +554,297 @@ __device__ int build_cta(const Args& A, const Seq& q, int si, double* sp, Run* s
     }
     double exc = __shfl_up_sync(FULL, inc, 1);
     if (lane == 0) exc = 0.0;
+    __syncthreads();  // s_red may still be read by a previous user
     if (lane == 31) s_red[warp] = inc;
     __syncthreads();
-    double wexc = 0.0, total = 0.0;
+    double wexc = 0.0, tot = 0.0;
     for (int w = 0; w < NW; ++w) {
         if (w < warp) wexc = dadd(wexc, s_red[w]);
-        total = dadd(total, s_red[w]);
+        tot = dadd(tot, s_red[w]);
     }
-    // look-back: publish this CTA's total, collect the totals of the CTAs before it
+    *total = tot;
+    return dadd(wexc, exc);
+}
+
+// All threads: this thread's run (two reference chains in the middle of the binade of `pred`,
+// the predicted start of its elements), then the warp pieces (one merged run when the
+// warp's 32 runs share a binade, else a table around the warp's predicted start). Ends with
+// __syncthreads.
+__device__ void runs_and_warp_pieces(const Scratch& S, const Seq& q, long long c0, int len, int E,
+                                     double pred, unsigned fl, const Smem& M, bool force_table = false) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int t0 = tid * E;
+    const int tl = max(0, min(E, len - t0));
+    const double* sp = M.sp;
+#ifdef MCR_XDOT_TIMING
+    const unsigned long long w_t0 = gtime();
+#endif
+    Run R = run_empty();
+    if (tl > 0) {
+        R.e = E_HARD;
+        const unsigned long long pb = bt(pred);
+        const int e = dexp(pb);
+        const int ng = (int)(pb >> 63);
+#ifndef XD_SKIP_CHAIN
+        if (e >= RUN_MIN_E && e <= 0x7f0 && !(fl & 2u)) {
+#else
+        if (false) {
+#endif
+            // reference starts: the predicted start itself (index made even) and its odd neighbour,
+            // so the chains follow the predicted trajectory
+            const double ref0 = fb(bt(pred) & ~1ull);
+            const double ref1 = fb(bt(ref0) + 1ull);
+            double s0 = ref0, s1 = ref1;
+            // extremes as bit patterns (one sign: they order like the magnitudes; a NaN or a sign
+            // change shows up as a different top-12-bit field and fails the binade test below)
+            unsigned long long a0 = bt(ref0), z0 = a0, a1 = bt(ref1), z1 = a1;
+#pragma unroll 4
+            for (int k = 0; k < tl; ++k) {
+                const double p = sp[t0 + k];
+                s0 = dadd(s0, p);
+                s1 = dadd(s1, p);
+                a0 = min(a0, bt(s0)); z0 = max(z0, bt(s0));
+                a1 = min(a1, bt(s1)); z1 = max(z1, bt(s1));
+            }
+            const bool same = (a0 >> 52) == (z0 >> 52) && (a1 >> 52) == (z1 >> 52) && (a0 >> 52) == (bt(ref0) >> 52);
+            // value extremes (for a negative binade the largest pattern is the smallest value)
+            const double mn0 = ng ? fb(z0) : fb(a0), mx0 = ng ? fb(a0) : fb(z0);
+            const double mn1 = ng ? fb(z1) : fb(a1), mx1 = ng ? fb(a1) : fb(z1);
+            // the chains model the run only if every partial sum stayed inside the binade, and
+            // are worth keeping only if they stayed clear of its ends by more than the prediction's
+            // error (4096 ulps); else the thread is summed element by element
+            const double margin = fb((unsigned long long)(e - 40) << 52);
+            const double bot = dadd(fb(((unsigned long long)e << 52) | 1ull), margin);
+            const double top = dsub(fb(((unsigned long long)e << 52) | MANT), margin);
+            const bool ok = same && (ng ? (-mx0 >= bot && -mn0 <= top && -mx1 >= bot && -mn1 <= top)
+                                        : (mn0 >= bot && mx0 <= top && mn1 >= bot && mx1 <= top));
+            if (ok) {
+                R.d[0] = dsub(s0, ref0); R.d[1] = dsub(s1, ref1);
+                R.lo[0] = dsub(mn0, ref0); R.hi[0] = dsub(mx0, ref0);
+                R.lo[1] = dsub(mn1, ref1); R.hi[1] = dsub(mx1, ref1);
+                R.e = e;
+                R.neg = ng;
+            }
+        }
+    }
+    M.runs[tid] = R;
+#ifdef MCR_XDOT_DEBUG
+    if (R.e != E_HARD && R.e != E_EMPTY) {
+        for (int t = 0; t < 3; ++t) {
+            double v = t == 0 ? pred : (t == 1 ? fb(bt(pred) + 1ull) : fb(bt(pred) + 2ull));
+            double lo = -INFINITY, hi = INFINITY, v0 = v;
+            int km = KM_NONE;
+            if (!run_apply(R, v, lo, hi, km)) continue;
+            stat(S, ST_DBG_RUN);
+            const double want = dbg_serial(q, c0 + t0, c0 + t0 + tl, v0);
+            if (!same_bits(want, v)) {
+                stat(S, ST_DBG_RUN_BAD);
+                if (S.stats) printf("xdot dbg: run e=%d neg=%d d0=%a d1=%a start=%a want=%a got=%a\n", R.e, R.neg, R.d[0], R.d[1], v0, want, v);
+            }
+        }
+    }
+#endif
+    if (R.e == E_HARD && S.stats) stat(S, ST_HARD);
+    __syncwarp();
+#ifdef MCR_XDOT_TIMING
+    const unsigned long long w_t1 = gtime();
+    if (lane == 0 && S.stats) atomicMax(S.stats + ST_W_CHAIN, w_t1 - w_t0);
+#endif
+    // Segments: maximal stretches of thread runs of one binade (a HARD thread is a segment of
+    // its own; trailing EMPTY threads join the segment before them). A segmented scan merges
+    // each segment into its last lane.
+    const int pe = __shfl_up_sync(FULL, R.e, 1), pn = __shfl_up_sync(FULL, R.neg, 1);
+    const bool head = lane == 0 || R.e == E_HARD || pe == E_HARD ||
+                      (R.e != E_EMPTY && pe != E_EMPTY && (R.e != pe || R.neg != pn));
+    const unsigned heads = __ballot_sync(FULL, head);
+    const int seg0 = 31 - __clz(heads & (FULL >> (31 - lane)));  // this lane's segment head
+    Run A = R;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        Run o;
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+            o.d[p] = __shfl_up_sync(FULL, A.d[p], off);
+            o.lo[p] = __shfl_up_sync(FULL, A.lo[p], off);
+            o.hi[p] = __shfl_up_sync(FULL, A.hi[p], off);
+        }
+        o.e = __shfl_up_sync(FULL, A.e, off);
+        o.neg = __shfl_up_sync(FULL, A.neg, off);
+        if (lane - off >= seg0) A = run_merge(o, A);
+    }
+    const unsigned ends = (heads >> 1) | 0x80000000u;  // last lane of each segment
+    const double wpred = __shfl_sync(FULL, pred, 0);
+    Desc* WD = M.wd + warp;
+    if (heads == 1u && __shfl_sync(FULL, A.e, 31) != E_HARD && !force_table) {
+        if (lane == 31) hdr_set_run(WD->h, A, wpred);
+#ifdef MCR_XDOT_TIMING
+        if (lane == 0 && S.stats) atomicMax(S.stats + ST_W_MERGE, gtime() - w_t1);
+#endif
+    } else {
+        if (S.stats && lane == 0) stat(S, ST_WARP_TABLE);
+        const unsigned long long mb0 = window_mb0(wpred);
+        const int wn = window_neg(wpred);
+        double v = cand(mb0, wn, lane), lo = -INFINITY, hi = INFINITY;
+        int km = KM_NONE;
+#ifdef XD_TWICE
+        for (int rep = 0; rep < 2; ++rep) {
+        const unsigned long long tr0 = gtime();
+        v = cand(mb0, wn, lane); lo = -INFINITY; hi = INFINITY; km = KM_NONE;
+#endif
+        int sl = 0;
+#ifdef MCR_XDOT_TIMING
+        int nfail = 0;
+        long long cyc_apply = 0, cyc_walk = 0;
+        const long long cyc_t0 = clock64();
+#endif
+        for (unsigned m = ends; m; m &= m - 1) {  // segment [sl, el]
+            const int el = __ffs(m) - 1;
+            Run G;
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {
+                G.d[p] = __shfl_sync(FULL, A.d[p], el);
+                G.lo[p] = __shfl_sync(FULL, A.lo[p], el);
+                G.hi[p] = __shfl_sync(FULL, A.hi[p], el);
+            }
+            G.e = __shfl_sync(FULL, A.e, el);
+            G.neg = __shfl_sync(FULL, A.neg, el);
+#ifdef MCR_XDOT_TIMING
+            const long long c_a = clock64();
+#endif
+            const bool okr = run_apply(G, v, lo, hi, km);
+#ifdef MCR_XDOT_TIMING
+            nfail += __popc(__ballot_sync(FULL, !okr));
+            const long long c_b = clock64();
+            cyc_apply += c_b - c_a;
+#endif
+            if (!okr)
+                lane_walk_threads(M.runs, sp, len, E, warp * 32 + sl, warp * 32 + el + 1, v, lo, hi, km,
+                                  S.stats ? S.stats + ST_SIMS_WARP : nullptr);
+#ifdef MCR_XDOT_TIMING
+            __syncwarp();
+            cyc_walk += clock64() - c_b;
+#endif
+            sl = el + 1;
+        }
+#ifdef XD_TWICE
+        if (lane == 0 && S.stats) atomicMax(S.stats + (rep == 0 ? ST_W_CHAIN : ST_W_MERGE), gtime() - tr0);
+        }
+#endif
+        LaneR Lx;
+        Lx.out = v; Lx.lo = lo; Lx.hi = hi; Lx.km = km;
+        Lx.hole = dexp(bt(v)) == 0x7ff ? 1 : 0;
+        store_lane(WD, lane, Lx);
+#ifdef MCR_XDOT_DEBUG
+        dbg_check_lane(S, q, c0 + warp * 32 * E, min(c0 + len, c0 + (long long)(warp + 1) * 32 * E), cand(mb0, wn, lane), load_lane(WD, lane), 1);
+#endif
+        if (lane == 0) hdr_set_table(WD->h, mb0, wn, wpred);
+#ifdef MCR_XDOT_TIMING
+        const int nhard = __popc(__ballot_sync(FULL, R.e == E_HARD));
+        if (lane == 0 && S.stats) {
+            const unsigned long long dt = gtime() - w_t1;
+            atomicMax(S.stats + ST_W_TABLE, dt);
+            // slowest table: time | segments | hard threads | warp | CTA range start
+            const long long cyc_all = clock64() - cyc_t0;
+            const unsigned long long info = (dt << 40) | ((unsigned long long)__popc(heads) << 32) |
+                ((unsigned long long)min((long long)(cyc_walk / 256), 255ll) << 24) |
+                ((unsigned long long)min((long long)(cyc_apply / 64), 255ll) << 16) |
+                (unsigned long long)min((long long)(cyc_all / 256), 65535ll);
+            atomicMax(S.stats + ST_W_SLOWEST, info);
+        }
+#endif
+    }
+    __syncthreads();
+}
+
+// Warp: the piece of L then R (both in shared memory; L covers threads [t0, t1), R threads
+// [t1, t2)) into *out (may be L): a merged run when both are runs of one binade, else a table
+// in L's window. With `walk`, lanes a piece does not serve walk its thread runs (the CTA's own
+// range is in shared memory); otherwise they become holes.
+__device__ void compose_pair(const Smem& M, int len, int E, const Desc* L, const Desc* R, Desc* out,
+                             int t0, int t1, int t2, bool walk) {
+    const int lane = threadIdx.x & 31;
+    const Hdr hl = L->h, hr = R->h;
+    if (hl.kind == K_RUN && hr.kind == K_RUN) {
+        const Run a = hdr_run(hl), b = hdr_run(hr);
+        if (runs_compatible(a, b)) {
+            __syncwarp();
+            if (lane == 0) hdr_set_run(out->h, run_merge(a, b), hl.pred);
+            __syncwarp();
+            return;
+        }
+    }
+    double v, lo = -INFINITY, hi = INFINITY;
+    int km = KM_NONE, hole = 0;
+    unsigned long long mb0;
+    int neg;
+    if (hl.kind == K_TABLE) {
+        const LaneR T = load_lane(L, lane);
+        v = T.out; lo = T.lo; hi = T.hi; km = T.km; hole = T.hole;
+        mb0 = hl.mb0; neg = hl.neg;
+    } else {
+        mb0 = window_mb0(hl.pred);
+        neg = window_neg(hl.pred);
+        v = cand(mb0, neg, lane);
+        if (!run_apply(hdr_run(hl), v, lo, hi, km)) {
+            if (walk) lane_walk_threads(M.runs, M.sp, len, E, t0, t1, v, lo, hi, km);
+            else hole = 1;
+        }
+    }
+    const PieceR P = load_piece(R);
+    if (!piece_apply_r(P, v, lo, hi, km) && !hole) {  // collective; then per lane
+        if (walk) lane_walk_threads(M.runs, M.sp, len, E, t1, t2, v, lo, hi, km);
+        else hole = 1;
+    }
+    LaneR Lx;
+    Lx.out = v; Lx.lo = lo; Lx.hi = hi; Lx.km = km;
+    Lx.hole = (hole || dexp(bt(v)) == 0x7ff) ? 1 : 0;
+    __syncwarp();  // every lane has read L
+    store_lane(out, lane, Lx);
+    if (lane == 0) hdr_set_table(out->h, mb0, neg, hl.pred);
+    __syncwarp();
+}
+
+// All threads: fold the NW pieces in p[0..NW) pairwise (level s merges p[2sw] and p[2sw + s]
+// into p[2sw]); the result is in p[0]. Piece i covers threads [32 i, 32 i + 32) when `walk`.
+__device__ void tree_fold(const Smem& M, int len, int E, Desc* p, bool walk) {
+    const int warp = threadIdx.x >> 5;
+    for (int s = 1; s < NW; s <<= 1) {
+        if (warp < NW / (2 * s)) {
+            const int a = 2 * s * warp, b = a + s;
+            compose_pair(M, len, E, p + a, p + b, p + a, a * 32, b * 32, (b + s) * 32, walk && s <= 2);
+        }
+        __syncthreads();
+    }
+}
+
+// Phase 1 of every CTA: take a ticket (the CTA's place in the sequence), build the CTA piece
+// around the predicted start (the sum of the totals of the CTAs before it: look-back) and
+// publish it. Returns the ticket.
+__device__ int build_cta(const Args& A, const Seq& q, int si, const Smem& M, double* s_red) {
+    const int tid = threadIdx.x;
+    const Scratch& S = A.S;
+    const int E = A.E;
+    __shared__ int s_tk;
+    __shared__ double s_pred;
+    XT_MARK(t_start);
+    if (tid == 0) s_tk = (int)atomicAdd(S.ticket + si, 1u);
+    __syncthreads();
+    const int ci = s_tk;
+    const int slot = q.cta0 + ci;
+    const long long c0 = q.a + (long long)ci * NT * E;
+    const long long c1 = min(q.b, c0 + (long long)NT * E);
+    const int len = (int)max(0ll, c1 - c0);
+    const unsigned fl = load_products(q, c0, len, M.sp);
+    XT_ADD(S, ST_T_LOAD, t_start);
+    XT_MARK(t_lb);
+    if (A.upto == 1) return ci;
+    double total;
+    const double exc = thread_scan(M.sp, len, E, s_red, &total);
     if (tid == 0) {
         S.lb_val[slot] = total;
         __threadfence();
         atomicExch(S.lb_flag + slot, 1);
-        if (s_fl) atomicOr(S.flags + si, s_fl);
+        if (fl) atomicOr(S.flags + si, fl);
     }
     double acc = 0.0;
     for (int j = tid; j < ci; j += NT) {
@@ -421,223 +859,217 @@ __device__ int build_cta(const Args& A, const Seq& q, int si, double* sp, Run* s
     if (tid == 0) s_pred = acc;
     __syncthreads();
     const double pred_cta = s_pred;
-    const double pred = dadd(pred_cta, dadd(wexc, exc));  // predicted start of this thread's elements
-    // pass 2: this thread's run
-    Run R;
-    R.d0 = R.d1 = R.x = 0.0;
-    R.neg = 0;
-    if (tl == 0) {
-        R.e = E_EMPTY;
-    } else {
-        R.e = E_HARD;
-        const unsigned long long pb = bt(pred);
-        const int e = dexp(pb);
-        const int ng = (int)(pb >> 63);
-        if (e >= RUN_MIN_E && e <= 0x7f0 && !(s_fl & 2u)) {
-            const double u = fb((unsigned long long)(e - 52) << 52);
-            const double X = __dadd_ru(ta, __dmul_ru((double)tl, u));
-            const double quarter = fb((unsigned long long)(e - 2) << 52);
-            const double margin = fb((unsigned long long)(e - 24) << 52);
-            const double lowlim = dadd(fb(((unsigned long long)e << 52) | 1ull), X);
-            const double highlim = dsub(fb(((unsigned long long)e << 52) | MANT), X);
-            const double ap = fabs(pred);
-            if (X < quarter && ap >= dadd(lowlim, margin) && ap <= dsub(highlim, margin)) {
-                const double ref0 = fb(((unsigned long long)ng << 63) | ((unsigned long long)e << 52) | (1ull << 51));
-                const double ref1 = fb(bt(ref0) + 1ull);
-                double s0 = ref0, s1 = ref1;
-                for (int k = 0; k < tl; ++k) {
-                    const double p = sp[t0 + k];
-                    s0 = dadd(s0, p);
-                    s1 = dadd(s1, p);
-                }
-                R.d0 = dsub(s0, ref0);
-                R.d1 = dsub(s1, ref1);
-                R.x = X;
-                R.e = e;
-                R.neg = ng;
-            }
-        }
-    }
-    s_runs[tid] = R;
-    S.runs[(size_t)slot * NT + tid] = R;
+    XT_ADD(S, ST_T_LOOKBACK, t_lb);
+    XT_MARK(t_runs);
+    if (A.upto == 2) return ci;
+    runs_and_warp_pieces(S, q, c0, len, E, dadd(pred_cta, exc), fl, M, A.upto == 13);
+    XT_ADD(S, ST_T_RUNS, t_runs);
+    XT_MARK(t_cta);
+    if (A.upto == 3 || A.upto == 13) return ci;
+    tree_fold(M, len, E, M.wd, true);  // the CTA piece, in wd[0]
+    if (S.stats && tid == 0 && M.wd[0].h.kind == K_TABLE) stat(S, ST_CTA_TABLE);
 #ifdef MCR_XDOT_DEBUG
-    if (R.e != E_HARD && R.e != E_EMPTY) {
-        for (int t = 0; t < 3; ++t) {
-            double v = t == 0 ? pred : (t == 1 ? fb(bt(pred) + 1ull) : fb(bt(pred) + 2ull));
-            double lo = -INFINITY, hi = INFINITY, v0 = v;
-            int km = KM_NONE;
-            if (!run_apply(R, v, lo, hi, km)) continue;
-            stat(S, ST_DBG_RUN);
-            const double want = dbg_serial(q, c0 + t0, c0 + t0 + tl, v0);
-            if (!same_bits(want, v)) {
-                stat(S, ST_DBG_RUN_BAD);
-                if (S.stats) printf("xdot dbg: run e=%d neg=%d d0=%a d1=%a x=%a start=%a want=%a got=%a\n", R.e, R.neg, R.d0, R.d1, R.x, v0, want, v);
-            }
-        }
-    }
+    if ((tid >> 5) == 0 && M.wd[0].h.kind == K_TABLE)
+        dbg_check_lane(S, q, c0, c0 + len, cand(M.wd[0].h.mb0, M.wd[0].h.neg, tid & 31), load_lane(M.wd, tid & 31), 2);
 #endif
-    if (R.e == E_HARD && tl > 0 && S.stats) stat(S, ST_HARD);
-    __syncwarp();
-    // warp piece: one merged run when all 32 thread runs share a binade, else a table
-    const int first = __ffs(__ballot_sync(FULL, R.e != E_EMPTY)) - 1;
-    const int e0 = __shfl_sync(FULL, R.e, max(first, 0));
-    const int n0 = __shfl_sync(FULL, R.neg, max(first, 0));
-    const bool same = R.e == E_EMPTY || (R.e != E_HARD && R.e == e0 && R.neg == n0);
-    const double wpred = __shfl_sync(FULL, pred, 0);
-    Desc* WD = s_wd + warp;
-    if (__all_sync(FULL, same)) {
-        Run M = R;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            Run o;
-            o.d0 = __shfl_down_sync(FULL, M.d0, off);
-            o.d1 = __shfl_down_sync(FULL, M.d1, off);
-            o.x = __shfl_down_sync(FULL, M.x, off);
-            o.e = __shfl_down_sync(FULL, M.e, off);
-            o.neg = __shfl_down_sync(FULL, M.neg, off);
-            if ((lane & (2 * off - 1)) == 0) M = run_merge(M, o);
-        }
-        if (lane == 0) hdr_set_run(WD->h, M, wpred);
-    } else {
-        if (S.stats && lane == 0) stat(S, ST_WARP_TABLE);
-        const unsigned long long mb0 = window_mb0(wpred);
-        const int wn = window_neg(wpred);
-        double v = cand(mb0, wn, lane), lo = -INFINITY, hi = INFINITY;
-        int km = KM_NONE;
-        for (int c = 0; c < 32; ++c) {
-            const Run Rc = s_runs[warp * 32 + c];
-            if (run_apply(Rc, v, lo, hi, km)) continue;
-            const int b0 = (warp * 32 + c) * E;
-            const int bl = max(0, min(E, len - b0));
-            for (int k = 0; k < bl; ++k) sim_step(v, sp[b0 + k], lo, hi, km);
-        }
-        Lane Lx;
-        Lx.out = v; Lx.lo = lo; Lx.hi = hi; Lx.km = km;
-        Lx.hole = dexp(bt(v)) == 0x7ff ? 1 : 0;
-        WD->l[lane] = Lx;
-#ifdef MCR_XDOT_DEBUG
-        dbg_check_lane(S, q, c0 + warp * 32 * E, min(c1, c0 + (long long)(warp + 1) * 32 * E), cand(mb0, wn, lane), Lx, 1);
-#endif
-        if (lane == 0) {
-            WD->h.kind = K_TABLE; WD->h.neg = wn; WD->h.e = 0; WD->h.mb0 = mb0; WD->h.pred = wpred;
-            WD->h.d0 = WD->h.d1 = WD->h.x = 0.0; WD->h.pad = 0; WD->h.pad2 = 0.0;
-        }
+    {  // publish
+        const double2* src = (const double2*)M.wd;
+        double2* dst = (double2*)(S.cta + slot);
+        for (int k = tid; k < (int)(sizeof(Desc) / 16); k += NT) dst[k] = src[k];
     }
-    __syncthreads();
-    // global copies of the warp pieces (fallback walks)
-    {
-        const int words = (int)(sizeof(Desc) / sizeof(double)) * NW;
-        const double* src = (const double*)s_wd;
-        double* dst = (double*)(S.warp + (size_t)slot * NW);
-        for (int k = tid; k < words; k += NT) dst[k] = src[k];
-    }
-    // CTA piece (warp 0)
-    if (warp == 0) {
-        bool allrun = true;
-        Run M;
-        M.e = E_EMPTY; M.neg = 0; M.d0 = M.d1 = M.x = 0.0;
-        for (int w = 0; w < NW; ++w) {
-            const Hdr& h = s_wd[w].h;
-            if (h.kind != K_RUN) { allrun = false; break; }
-            const Run r = hdr_run(h);
-            if (!runs_compatible(M, r)) { allrun = false; break; }
-            M = run_merge(M, r);
-        }
-        Desc* CD = S.cta + slot;
-        if (allrun) {
-            if (lane == 0) hdr_set_run(CD->h, M, pred_cta);
-        } else {
-            if (S.stats && lane == 0) stat(S, ST_CTA_TABLE);
-            const unsigned long long mb0 = window_mb0(pred_cta);
-            const int cn = window_neg(pred_cta);
-            double v = cand(mb0, cn, lane), lo = -INFINITY, hi = INFINITY;
-            int km = KM_NONE;
-            int hole = 0;
-            for (int w = 0; w < NW; ++w) {
-                const bool ok = piece_apply(s_wd + w, v, lo, hi, km);  // collective
-                hole |= ok ? 0 : 1;
-            }
-            Lane Lx;
-            Lx.out = v; Lx.lo = lo; Lx.hi = hi; Lx.km = km;
-            Lx.hole = (hole || dexp(bt(v)) == 0x7ff) ? 1 : 0;
-            CD->l[lane] = Lx;
-#ifdef MCR_XDOT_DEBUG
-            dbg_check_lane(S, q, c0, c1, cand(mb0, cn, lane), Lx, 2);
-#endif
-            if (lane == 0) {
-                CD->h.kind = K_TABLE; CD->h.neg = cn; CD->h.e = 0; CD->h.mb0 = mb0; CD->h.pred = pred_cta;
-                CD->h.d0 = CD->h.d1 = CD->h.x = 0.0; CD->h.pad = 0; CD->h.pad2 = 0.0;
-            }
-        }
-    }
+    XT_ADD(S, ST_T_CTA, t_cta);
     return ci;
 }
 
-// The last CTA of a sequence: compose the CTA pieces and walk the true value from 0.0.
-__device__ double root(const Args& A, const Seq& q, int si, Desc* s_gd) {
+// All threads of the root: the exact sum of CTA range ci from its true start (*s_v),
+// rebuilding the range's pieces around that start (the predictions are then exact up to the
+// rounding inside the range) and walking them with warp 0; a warp piece that still does not
+// apply is replaced by its thread runs, a thread run by its elements.
+__device__ void rebuild_walk(const Args& A, const Seq& q, int ci, const Smem& M, double* s_red, double* s_v) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int E = A.E;
+    const long long c0 = q.a + (long long)ci * NT * E;
+    const long long c1 = min(q.b, c0 + (long long)NT * E);
+    const int len = (int)max(0ll, c1 - c0);
+    if (threadIdx.x == 0) stat(A.S, ST_CTA_FB);
+    __syncthreads();  // sp / runs / wd may still be read
+    const double v0 = *s_v;
+    const unsigned fl = load_products(q, c0, len, M.sp);
+    double total;
+    const double exc = thread_scan(M.sp, len, E, s_red, &total);
+    runs_and_warp_pieces(A.S, q, c0, len, E, dadd(v0, exc), fl, M);
+    if (warp == 0) {
+        double v = v0;
+        for (int w = 0; w < NW; ++w) {
+            const PieceR P = load_piece(M.wd + w);
+            double lo = -INFINITY, hi = INFINITY;
+            int km = KM_NONE;
+            if (piece_apply_r(P, v, lo, hi, km)) continue;
+            if (lane == 0) stat(A.S, ST_WARP_FB);
+            for (int t = w * 32; t < w * 32 + 32; ++t) {  // uniform scalar walk
+                const Run R = M.runs[t];
+                if (run_apply(R, v, lo, hi, km)) continue;
+                if (lane == 0) stat(A.S, ST_CHUNK_FB);
+                const int b0 = t * E, bl = max(0, min(E, len - b0));
+                for (int k = 0; k < bl; ++k) v = dadd(v, M.sp[b0 + k]);
+            }
+        }
+        if (lane == 0) *s_v = v;
+    }
+    __syncthreads();
+}
+
+// All threads of the root: carry the true value (*s_v) through the staged CTA pieces
+// [c0, c1) (the stage holds pieces from index b0), rebuilding the ones it cannot use.
+__device__ void walk_ctas(const Args& A, const Seq& q, int b0, int c0, int c1, const Smem& M,
+                          double* s_red, double* s_v) {
+    __shared__ int s_c;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int c = c0;
+    while (c < c1) {
+        __syncthreads();
+        if (warp == 0) {
+            double v = *s_v;
+            int cc = c;
+            for (; cc < c1; ++cc) {
+                const PieceR P = load_piece(M.stage + (cc - b0));
+                double lo = -INFINITY, hi = INFINITY;
+                int km = KM_NONE;
+#ifdef MCR_XDOT_DEBUG
+                const double v_in = v;
+#endif
+                if (!piece_apply_r(P, v, lo, hi, km)) {
+#ifdef MCR_XDOT_DEBUG
+                    why_failed(A.S, M.stage + (cc - b0), v_in);
+#endif
+                    break;
+                }
+            }
+            if (lane == 0) { *s_v = v; s_c = cc; }
+        }
+        __syncthreads();
+        c = s_c;
+        if (c >= c1) break;
+        rebuild_walk(A, q, c, M, s_red, s_v);
+        ++c;
+    }
+    __syncthreads();
+}
+
+// The last CTA of a sequence: the sequence's sum, from the exact start 0.0.
+__device__ double root(const Args& A, const Seq& q, int si, const Smem& M, double* s_red) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const Scratch& S = A.S;
     const int n = q.ncta;
-    const int Q = (n + NW - 1) / NW;
     __shared__ double s_v;
-    __shared__ int s_nf;
-    if (threadIdx.x == 0) s_nf = (int)((__ldcg((const int*)S.flags + si) >> 1) & 1);
+    __shared__ int s_nf, s_ok;
+    XT_MARK(t_root);
+    if (threadIdx.x == 0) {
+        s_nf = (int)((__ldcg((const int*)S.flags + si) >> 1) & 1);
+        s_v = 0.0;
+    }
     __syncthreads();
     if (s_nf) {  // a non-finite product: the reference's IEEE chain, element by element
         if (warp == 0) {
-            stat(S, ST_SERIAL);
+            if (lane == 0) stat(S, ST_SERIAL);
             double v = 0.0;
-            for (long long i = q.a; i < q.b; ++i) v = dadd(v, dmul(__ldcg(q.u + i), __ldcg(q.v + i)));
+            for (long long i0 = q.a; i0 < q.b; i0 += 32) {
+                const int cnt = (int)min(32ll, q.b - i0);
+                const double p = lane < cnt ? dmul(__ldcg(q.u + i0 + lane), __ldcg(q.v + i0 + lane)) : 0.0;
+                for (int k = 0; k < cnt; ++k) v = dadd(v, __shfl_sync(FULL, p, k));
+            }
             if (lane == 0) s_v = v;
         }
         __syncthreads();
         return s_v;
     }
-    // groups 1..NW-1: tables over Q consecutive CTA pieces
-    if (warp > 0) {
-        const int g0 = warp * Q, g1 = min(n, g0 + Q);
-        Desc* G = s_gd + warp;
-        if (g0 < g1) {
-            const double gp = __ldcg(&S.cta[q.cta0 + g0].h.pred);
-            const unsigned long long mb0 = window_mb0(gp);
-            const int gn = window_neg(gp);
-            double v = cand(mb0, gn, lane), lo = -INFINITY, hi = INFINITY;
-            int km = KM_NONE, hole = 0;
-            for (int c = g0; c < g1; ++c) {
-                const bool ok = piece_apply(S.cta + q.cta0 + c, v, lo, hi, km);
-                hole |= ok ? 0 : 1;
-            }
-            Lane Lx;
-            Lx.out = v; Lx.lo = lo; Lx.hi = hi; Lx.km = km;
-            Lx.hole = (hole || dexp(bt(v)) == 0x7ff) ? 1 : 0;
-            G->l[lane] = Lx;
-#ifdef MCR_XDOT_DEBUG
-            dbg_check_lane(S, q, q.a + (long long)g0 * NT * A.E, min(q.b, q.a + (long long)g1 * NT * A.E), cand(mb0, gn, lane), Lx, 3);
-#endif
-            if (lane == 0) {
-                G->h.kind = K_TABLE; G->h.neg = gn; G->h.e = 0; G->h.mb0 = mb0; G->h.pred = gp;
-            }
-        }
-    } else {
-        // group 0 from the exact start
-        double v = 0.0;
-        for (int c = 0; c < min(n, Q); ++c) walk_cta(A, q, c, v);
-        if (lane == 0) s_v = v;
+    __shared__ __align__(8) uint64_t s_bar;
+    if (threadIdx.x == 0) {
+        mbar_init(&s_bar, 1);
+        mbar_fence_init();
     }
     __syncthreads();
-    if (warp == 0) {
-        double v = s_v;
-        for (int g = 1; g < NW; ++g) {
-            const int g0 = g * Q, g1 = min(n, g0 + Q);
-            if (g0 >= g1) break;
-            if (piece_scalar(s_gd + g, v)) continue;
-            stat(S, ST_GROUP_FB);
-            for (int c = g0; c < g1; ++c) walk_cta(A, q, c, v);
+    uint32_t phase = 0;
+    for (int b0 = 0; b0 < n; b0 += A.stage) {
+        const int b1 = min(n, b0 + A.stage);
+        // stage the batch's CTA pieces: one bulk copy (the pieces were written through the
+        // generic proxy by other CTAs; the stage may have been read by this one)
+        if (threadIdx.x == 0) {
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            fence_proxy_async();
+            const uint32_t bytes = (uint32_t)(sizeof(Desc) * (size_t)(b1 - b0));
+            mbar_expect_tx(&s_bar, bytes);
+            bulk_g2s(M.stage, S.cta + q.cta0 + b0, bytes, &s_bar);
         }
-        // cumsum starts from p_0 itself: -0.0 survives only when every product is -0.0
-        if (v == 0.0 && q.b > q.a && !(__ldcg((const int*)S.flags + si) & 1)) v = -0.0;
-        if (lane == 0) s_v = v;
+        mbar_wait(&s_bar, phase);
+        phase ^= 1u;
+        const int Q = (b1 - b0 + NW - 1) / NW;
+        {  // group tables: warp g composes staged pieces [b0 + g Q, ...)
+            const int g0 = b0 + warp * Q, g1 = min(b1, g0 + Q);
+            Desc* G = M.gd + warp;
+            if (g0 < g1) {
+                const double gp = M.stage[g0 - b0].h.pred;
+                const unsigned long long mb0 = window_mb0(gp);
+                const int gn = window_neg(gp);
+                double v = cand(mb0, gn, lane), lo = -INFINITY, hi = INFINITY;
+                int km = KM_NONE, hole = 0;
+                for (int c = g0; c < g1; ++c) hole |= piece_apply_r(load_piece(M.stage + (c - b0)), v, lo, hi, km) ? 0 : 1;
+                LaneR Lx;
+                Lx.out = v; Lx.lo = lo; Lx.hi = hi; Lx.km = km;
+                Lx.hole = (hole || dexp(bt(v)) == 0x7ff) ? 1 : 0;
+                store_lane(G, lane, Lx);
+#ifdef MCR_XDOT_DEBUG
+                dbg_check_lane(S, q, q.a + (long long)g0 * NT * A.E, min(q.b, q.a + (long long)g1 * NT * A.E), cand(mb0, gn, lane), load_lane(G, lane), 3);
+#endif
+                if (lane == 0) hdr_set_table(G->h, mb0, gn, gp);
+            } else if (lane == 0) {
+                hdr_set_run(G->h, run_empty(), 0.0);  // identity
+            }
+            __syncwarp();
+            const double2* src = (const double2*)G;
+            double2* dst = (double2*)(M.td + warp);
+            for (int k = lane; k < (int)(sizeof(Desc) / 16); k += 32) dst[k] = src[k];
+        }
+        __syncthreads();
+        tree_fold(M, 0, A.E, M.td, false);
+        XT_ADD(S, ST_T_ROOT_GROUPS, t_root);
+        XT_MARK(t_walk);
+        if (warp == 0) {  // the whole batch from the true value
+            double v = s_v, lo = -INFINITY, hi = INFINITY;
+            int km = KM_NONE;
+            const bool ok = piece_apply_r(load_piece(M.td), v, lo, hi, km);
+            if (lane == 0) {
+                s_ok = ok;
+                if (ok) s_v = v;
+            }
+        }
+        __syncthreads();
+        if (!s_ok) {  // group by group; a group that does not apply, CTA piece by CTA piece
+            for (int g = 0; g < NW; ++g) {
+                const int g0 = b0 + g * Q, g1 = min(b1, g0 + Q);
+                if (g0 >= g1) break;
+                if (warp == 0) {
+                    double v = s_v, lo = -INFINITY, hi = INFINITY;
+                    int km = KM_NONE;
+                    const bool ok = piece_apply_r(load_piece(M.gd + g), v, lo, hi, km);
+                    if (lane == 0) {
+                        s_ok = ok;
+                        if (ok) s_v = v;
+                    }
+                }
+                __syncthreads();
+                if (!s_ok) {
+                    if (threadIdx.x == 0) stat(S, ST_GROUP_FB);
+                    walk_ctas(A, q, b0, g0, g1, M, s_red, &s_v);
+                }
+            }
+        }
+        XT_ADD(S, ST_T_ROOT_WALK, t_walk);
+        __syncthreads();
     }
+    // cumsum starts from p_0 itself: -0.0 survives only when every product is -0.0
+    if (threadIdx.x == 0 && s_v == 0.0 && q.b > q.a && !(__ldcg((const int*)S.flags + si) & 1)) s_v = -0.0;
+    if (threadIdx.x == 0) stat(S, ST_T_LAUNCHES);
     __syncthreads();
     return s_v;
 }
@@ -662,23 +1094,36 @@ __device__ __forceinline__ int find_seq(const Seq* seqs, int nseq, int cta) {
     return lo;
 }
 
-// Shared memory: NT*E products, NT thread runs, NW warp pieces (also the root's group tables).
-__host__ __device__ constexpr size_t smem_bytes(int E) {
-    return sizeof(double) * (size_t)NT * (size_t)E + sizeof(Run) * NT + sizeof(Desc) * NW;
-}
-
 // Per-launch body. Returns true in the one CTA that finished the last sequence, with the
 // dots (block partials combined when pardots) in d[0], d[1]; thread 0 only.
 __device__ bool xdot_body(const Args& A, double* d) {
     extern __shared__ __align__(16) unsigned char xsm[];
-    double* sp = (double*)xsm;
-    Run* s_runs = (Run*)(xsm + sizeof(double) * (size_t)NT * (size_t)A.E);
-    Desc* s_wd = (Desc*)(s_runs + NT);
+    const Smem M = smem_layout(xsm, A.E);
     __shared__ double s_red[NW];
     __shared__ int s_flag;
     const int si = find_seq(A.seqs, A.nseq, blockIdx.x);
     const Seq q = A.seqs[si];
-    build_cta(A, q, si, sp, s_runs, s_wd, s_red);
+#ifdef MCR_XDOT_TIMING
+    if (threadIdx.x == 0 && A.S.stats) {
+        const unsigned long long t = gtime();
+        atomicMin(A.S.stats + ST_G_MIN_ENTRY, t);
+        atomicMax(A.S.stats + ST_G_MAX_ENTRY, t);
+    }
+#endif
+    build_cta(A, q, si, M, s_red);
+    if ((A.upto >= 1 && A.upto <= 4) || A.upto == 13) {  // diagnostics: the build phases alone
+        __syncthreads();
+        if (threadIdx.x == 0 && atomicAdd(A.S.done + si, 1u) == (unsigned)(q.ncta - 1)) {
+            A.S.ticket[si] = 0u;
+            A.S.done[si] = 0u;
+            A.S.flags[si] = 0u;
+            for (int j = 0; j < q.ncta; ++j) A.S.lb_flag[q.cta0 + j] = 0;
+        }
+        return false;
+    }
+#ifdef MCR_XDOT_TIMING
+    if (threadIdx.x == 0 && A.S.stats) atomicMax(A.S.stats + ST_G_MAX_BUILD, gtime());
+#endif
     // the last CTA of the sequence composes it
     __threadfence();
     __syncthreads();
@@ -686,7 +1131,31 @@ __device__ bool xdot_body(const Args& A, double* d) {
     __syncthreads();
     if (!s_flag) return false;
     __threadfence();
-    const double r = root(A, q, si, s_wd);
+#ifdef MCR_XDOT_TIMING
+    const unsigned long long g_root0 = gtime();
+#endif
+    const double r = root(A, q, si, M, s_red);
+#ifdef MCR_XDOT_TIMING
+    if (threadIdx.x == 0 && A.S.stats && A.nseq == 1) {
+        unsigned long long* T = A.S.stats;
+        const unsigned long long g1 = gtime(), mn = T[ST_G_MIN_ENTRY], mxe = T[ST_G_MAX_ENTRY], mb = T[ST_G_MAX_BUILD];
+        T[ST_G_SKEW] += mxe - mn;
+        T[ST_G_BUILD] += mb - mn;
+        T[ST_G_ROOT] += g1 - g_root0;
+        T[ST_G_TOTAL] += g1 - mn;
+        T[ST_G_MIN_ENTRY] = ~0ull;
+        T[ST_G_MAX_ENTRY] = 0ull;
+        T[ST_G_MAX_BUILD] = 0ull;
+        for (int k = 0; k < 4; ++k) {
+            T[ST_MS_LOAD + k] += T[ST_M_LOAD + k];
+            T[ST_M_LOAD + k] = 0ull;
+        }
+        for (int k = 0; k < 3; ++k) {
+            T[ST_WS_CHAIN + k] += T[ST_W_CHAIN + k];
+            T[ST_W_CHAIN + k] = 0ull;
+        }
+    }
+#endif
     if (threadIdx.x == 0) A.S.result[si] = r;
     reset_seq(A, q, si);
     // the last sequence combines
@@ -718,9 +1187,6 @@ __device__ bool xdot_body(const Args& A, double* d) {
 }
 
 }  // namespace xd
-}  // namespace mcr
-
-namespace mcr {
 
 // Reference-order dots of one BiCGStab reduction point (W = SQ_S0 / SQ_V / SQ_T / SQ_E), or
 // the test entry (W = SQ_TEST: results to A.out, no solver state).

@@ -15,6 +15,7 @@ struct XdotCtx {
         int nseq = 0, nseq0 = 0, ndot = 1, pardots = 0, grid = 0, E = 1, nblocks = 1;
         const double* key[4] = {nullptr, nullptr, nullptr, nullptr};
         size_t smem = 0;
+        int stage = 1;
         int64_t n = -1;
     } plan[5];
     std::vector<void*> seq_bufs;
@@ -35,6 +36,20 @@ inline void row_blocks(int64_t n, int k, std::vector<int64_t>& lo, std::vector<i
     }
 }
 
+// dynamic shared memory a k_xdot CTA may use: the opt-in maximum less the kernel's static part
+inline int xdot_smem_max() {
+    static int v = 0;
+    if (v) return v;
+    int dev = 0, optin = 227 * 1024;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa{};
+    int stat_bytes = 1024;
+    if (cudaFuncGetAttributes(&fa, k_xdot<SQ_TEST>) == cudaSuccess) stat_bytes = (int)fa.sharedSizeBytes;
+    v = optin - stat_bytes - 256;
+    return v;
+}
+
 inline int sm_count(int device) {
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
@@ -45,8 +60,7 @@ template <int W>
 int xdot_smem_attr() {
     static int done = 0;
     if (done) return MCR_OK;
-    CK(cudaFuncSetAttribute(k_xdot<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)xd::smem_bytes(xd::EMAX)));
+    CK(cudaFuncSetAttribute(k_xdot<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, xdot_smem_max()));
     done = 1;
     return MCR_OK;
 }
@@ -65,10 +79,18 @@ int xdot_plan(XdotCtx& X, int w, cudaStream_t s, int device, int64_t n, int ndot
     row_blocks(n, nb, lo, hi);
     const int nsm = sm_count(device);
     const int64_t total = (int64_t)ndot * n;
+    // one CTA per SM (the shared memory is sized for that): the smallest odd E whose grid fits
     int64_t E = (total + (int64_t)xd::NT * nsm - 1) / ((int64_t)xd::NT * nsm);
-    E = std::max<int64_t>(1, std::min<int64_t>(E, xd::EMAX));
-    if (const char* env = std::getenv("MCR_XDOT_E")) E = std::max(1, std::min(xd::EMAX, std::atoi(env)));
-    E |= 1;
+    E = std::max<int64_t>(1, std::min<int64_t>(E, xd::EMAX)) | 1;
+    auto grid_of = [&](int64_t e) {
+        int64_t g = 0;
+        for (int k = 0; k < ndot; ++k)
+            for (int b = 0; b < nb; ++b)
+                g += std::max<int64_t>(1, (hi[b] - lo[b] + (int64_t)xd::NT * e - 1) / ((int64_t)xd::NT * e));
+        return g;
+    };
+    while (E + 2 <= xd::EMAX && grid_of(E) > nsm) E += 2;
+    if (const char* env = std::getenv("MCR_XDOT_E")) E = std::max(1, std::min(xd::EMAX, std::atoi(env))) | 1;
     const int64_t per = (int64_t)xd::NT * E;
     std::vector<xd::Seq> seqs;
     int grid = 0;
@@ -88,8 +110,7 @@ int xdot_plan(XdotCtx& X, int w, cudaStream_t s, int device, int64_t n, int ndot
     const int nseq = (int)seqs.size();
     if (grid > X.grid_cap || nseq > X.nseq_cap) {
         const int gc = std::max(grid, X.grid_cap), sc = std::max(nseq, X.nseq_cap);
-        const size_t bytes = sizeof(xd::Desc) * (size_t)gc * (1 + xd::NW) +
-                             sizeof(xd::Run) * (size_t)gc * xd::NT + sizeof(double) * (size_t)gc +
+        const size_t bytes = sizeof(xd::Desc) * (size_t)gc + sizeof(double) * (size_t)gc +
                              sizeof(int) * (size_t)gc + sizeof(double) * (size_t)sc +
                              sizeof(unsigned) * (size_t)(3 * sc + 1) + 256;
         if (X.blk) CK(cudaFreeAsync(X.blk, s));
@@ -99,8 +120,6 @@ int xdot_plan(XdotCtx& X, int w, cudaStream_t s, int device, int64_t n, int ndot
         char* p = (char*)X.blk;
         auto take = [&](size_t b) { char* r = p; p += (b + 15) & ~(size_t)15; return r; };
         X.S.cta = (xd::Desc*)take(sizeof(xd::Desc) * (size_t)gc);
-        X.S.warp = (xd::Desc*)take(sizeof(xd::Desc) * (size_t)gc * xd::NW);
-        X.S.runs = (xd::Run*)take(sizeof(xd::Run) * (size_t)gc * xd::NT);
         X.S.lb_val = (double*)take(sizeof(double) * (size_t)gc);
         X.S.result = (double*)take(sizeof(double) * (size_t)sc);
         X.S.lb_flag = (int*)take(sizeof(int) * (size_t)gc);
@@ -114,6 +133,9 @@ int xdot_plan(XdotCtx& X, int w, cudaStream_t s, int device, int64_t n, int ndot
     if (!X.stats && std::getenv("MCR_XDOT_STATS")) {
         CK(cudaMallocAsync((void**)&X.stats, sizeof(unsigned long long) * xd::ST_COUNT, s));
         CK(cudaMemsetAsync(X.stats, 0, sizeof(unsigned long long) * xd::ST_COUNT, s));
+        const unsigned long long big = ~0ull;
+        CK(cudaMemcpyAsync(X.stats + xd::ST_G_MIN_ENTRY, &big, sizeof(big), cudaMemcpyHostToDevice, s));
+        CK(cudaStreamSynchronize(s));
     }
     X.S.stats = X.stats;
     if (P.d_seqs) CK(cudaFreeAsync(P.d_seqs, s));
@@ -127,7 +149,12 @@ int xdot_plan(XdotCtx& X, int w, cudaStream_t s, int device, int64_t n, int ndot
     P.nblocks = nblocks;
     P.grid = grid;
     P.E = (int)E;
-    P.smem = xd::smem_bytes((int)E);
+    // the root stages its sequence's CTA pieces in shared memory (in batches if they do not fit)
+    int maxc = 1;
+    for (const auto& q : seqs) maxc = std::max(maxc, q.ncta);
+    const int room = (int)(((size_t)xdot_smem_max() - xd::smem_bytes((int)E, 0)) / sizeof(xd::Desc));
+    P.stage = std::max(1, std::min(maxc, room));
+    P.smem = xd::smem_bytes((int)E, P.stage);
     P.n = n;
     std::copy(key, key + 4, P.key);
     return MCR_OK;
@@ -142,6 +169,9 @@ xd::Args xdot_args(const XdotCtx& X, int w, double* out) {
     A.ndot = P.ndot;
     A.pardots = P.pardots;
     A.E = P.E;
+    A.stage = P.stage;
+    static const int upto = std::getenv("MCR_XDOT_UPTO") ? std::atoi(std::getenv("MCR_XDOT_UPTO")) : 0;
+    A.upto = upto;
     A.S = X.S;
     A.out = out;
     return A;

@@ -19,7 +19,14 @@ XDOT_STATS = ("hard_threads", "warp_tables", "cta_tables", "group_fallbacks", "c
               "warp_fallbacks", "thread_fallbacks", "serial_sums",
               # self-checks of a MCR_XDOT_DEBUG build
               "dbg_runs", "dbg_runs_bad", "dbg_tables", "dbg_tables_bad", "dbg_translations",
-              "dbg_translations_bad", "dbg_spare")
+              "dbg_translations_bad", "dbg_spare",
+              "why_hole", "why_sign", "why_binade", "why_slack", "why_modulus", "why_run_binade",
+              "why_run_bounds",
+              "t_load", "t_lookback", "t_runs_warps", "t_cta", "t_root_groups", "t_root_walk",
+              "t_roots", "ns_skew", "ns_build", "ns_root", "ns_total", "_min_entry", "_max_entry",
+              "_max_build", "_m_load", "_m_lookback", "_m_runs", "_m_cta", "maxns_load",
+              "maxns_lookback", "maxns_runs", "maxns_cta", "lane_sims_warp", "lane_sims_cta",
+              "_w_chain", "_w_merge", "_w_table", "maxns_chain", "maxns_merge", "maxns_table", "slowest_table")
 
 
 def _run(u, v, nblocks: int, device: int, stats: bool):

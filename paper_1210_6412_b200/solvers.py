@@ -203,10 +203,11 @@ class DeviceMatrix:
         return out.value
 
     def solve(self, method: str, b: np.ndarray, x0: Optional[np.ndarray], tol: float,
-              max_it: int, dots: str = "tree"):
+              max_it: int, dots: str = "sequential", dot_blocks: int = 1):
         fn = {"jacobi": self._L.mcr_jacobi, "bicgstab": self._L.mcr_bicgstab}[method]
-        mode = _lib.DOTS_SEQUENTIAL if dots == "sequential" else _lib.DOTS_TREE
-        rc = self._L.mcr_set_dot_mode(self._h, mode)
+        rc = self._L.mcr_set_dot_mode(self._h, _lib.DOT_MODES[dots])
+        if rc == _lib.MCR_OK:
+            rc = self._L.mcr_set_dot_blocks(self._h, int(dot_blocks))
         if rc != _lib.MCR_OK:
             _raise_native(rc)
         b = np.ascontiguousarray(b, dtype=np.float64)
