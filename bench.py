@@ -7,7 +7,7 @@ dominant system n = 1e6, nnz = 1e7 (GenSpec(n=10**6, nnz=10**7, seed=trial_seed(
 None, 1e7, 0)), bit-identical to mcreach.generate_dd_matrix) with rhs generate_rhs(n, seed).
 One step = one Jacobi solve + one BiCGStab solve from x0 = 0 to tol 1e-10, each including
 its final true residual. Metric value = solves per second over the whole job (N replicas at
-N > 1: the C2 system fits one GPU and does not shard, "replicas only" in DESIGN.md).
+N > 1 the system's rows shard over the N GPUs: strong scaling of one solve, run_sharded).
 
 Our arm: inputs resident in HBM (device-pointer C ABI), L2 flushed (512 MiB write) before
 every step, CUDA events on the stream the library launches on, barrier + synchronize around
@@ -273,7 +273,7 @@ def run_ours(args):
 
     dm = DeviceMatrix(m, local)
     L.mcr_set_stream(dm.handle, ctypes.c_void_p(stream.cuda_stream))
-    L.mcr_set_dot_mode(dm.handle, _lib.DOTS_TREE)
+    L.mcr_set_dot_mode(dm.handle, _lib.DOT_MODES[args.dots])
     b_dev = torch.from_numpy(b).to(dev)
     x_dev = torch.empty(n, dtype=torch.float64, device=dev)
     y_dev = torch.empty(n, dtype=torch.float64, device=dev)
@@ -325,6 +325,21 @@ def run_ours(args):
         dist.barrier()
     value = 2.0 * world * args.steps / (total_ms / 1e3)
 
+    # ---- the opt-in tree-dot BiCGStab on the same handle (not the reference's order)
+    other = None
+    if args.dots != "tree":
+        L.mcr_set_dot_mode(dm.handle, _lib.DOTS_TREE)
+        tms, trep = [], None
+        for i in range(args.warmup + 3):
+            flush.zero_()
+            trep = solve(L.mcr_bicgstab_device)
+            if i >= args.warmup:
+                tms.append(trep.device_seconds * 1e3)
+        L.mcr_set_dot_mode(dm.handle, _lib.DOT_MODES[args.dots])
+        other = {"dots": "tree (fused fixed-shape trees; not the reference's summation order)",
+                 "bicgstab_ms": statistics.median(tms), "bicgstab_iterations": int(trep.iterations),
+                 "step_ms_estimate": statistics.median(jac_ms) + statistics.median(tms)}
+
     # ---- dominant kernel alone: CSR SpMV (k_spmv) with CUDA events, L2 flushed
     spmv_ms = []
     xin = torch.rand(n, dtype=torch.float64, device=dev)
@@ -361,7 +376,48 @@ def run_ours(args):
                   "frac": ab["spmv"] / spmv_s / 1e9 / peak,
                   "how": "one M x launch, L2 flushed (512 MiB write) before each, CUDA events"}
 
-    # ---- end to end through the public API with pinned host buffers
+    # ---- end to end through the drop-in: the reference's registry with the GPU methods
+    # installed (plugin.install()), a fresh reference CsrMatrix over pageable numpy arrays every
+    # step (so every step uploads the matrix), b from the host, x back to the host: exactly
+    # what `SOLVERS["jacobi-gpu"](m, b)` costs a reference caller
+    from paper_1210_6412_b200 import plugin
+    from paper_1210_6412_b200 import solvers as gsolvers
+    ms = reference_module()
+    if ms is not None:
+        from mcreach import CsrMatrix as RefCsr
+        reg = dict(ms.SOLVERS)
+        plugin.install(reg)
+        make_csr = RefCsr
+        via = "mcreach.solvers.SOLVERS with plugin.install() (reference CsrMatrix, pageable numpy)"
+    else:
+        reg = gsolvers.SOLVERS
+        make_csr = CsrMatrix
+        via = "paper_1210_6412_b200.solvers.SOLVERS (no mcreach importable; pageable numpy)"
+    gcfg = gsolvers.SolverConfig(dot_products=args.dots, device=local)
+    rs_p, col_p, val_p, b_p = (np.array(m.rstart), np.array(m.col), np.array(m.nonzero), np.array(b))
+    e2e_s = []
+    for i in range(args.warmup + args.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        mat = make_csr(n, rs_p, col_p, val_p)        # a new object: the drop-in uploads it
+        rj_e = reg["jacobi-gpu"](mat, b_p, gcfg)
+        rb_e = reg["bicgstab-gpu"](mat, b_p, gcfg)
+        del mat
+        gsolvers._cache.clear()                       # release the device copy every step
+        torch.cuda.synchronize()
+        if i >= args.warmup:
+            e2e_s.append(time.perf_counter() - t0)
+    e2e_total = sum(e2e_s)
+    if dist:
+        t = torch.tensor([e2e_total], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_total = float(t.item())
+    e2e_value = 2.0 * world * args.steps / e2e_total
+    e2e_iters = {"jacobi": int(rj_e.iterations), "bicgstab": int(rb_e.iterations)}
+    h2d = 8 * (n + 1) + 8 * nnz + 8 * nnz + 2 * 8 * n
+    d2h = 2 * 8 * n
+
+    # the same through the device handle API with pinned host buffers (sub-record)
     def pinned(a):
         t = torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
         return t, t.numpy()
@@ -372,11 +428,12 @@ def run_ours(args):
     _b_t, b_h = pinned(b)
     _x_t, x_h = pinned(np.zeros(n))
     hm = CsrMatrix(n, rs_h, col_h, val_h)
-    e2e_s = []
-    for i in range(args.warmup + args.steps):
+    pin_s = []
+    for i in range(1 + args.steps):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         h = DeviceMatrix(hm, local)             # H2D: rowptr, col, val
+        L.mcr_set_dot_mode(h.handle, _lib.DOT_MODES[args.dots])
         for method in ("jacobi", "bicgstab"):   # H2D: b; D2H: x
             fn = L.mcr_jacobi if method == "jacobi" else L.mcr_bicgstab
             rep = _lib.Report()
@@ -385,16 +442,9 @@ def run_ours(args):
             assert rc in (_lib.MCR_OK, _lib.MCR_NOT_CONVERGED), _lib.last_error()
         h.close()
         torch.cuda.synchronize()
-        if i >= args.warmup:
-            e2e_s.append(time.perf_counter() - t0)
-    e2e_total = sum(e2e_s)
-    if dist:
-        t = torch.tensor([e2e_total], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_total = float(t.item())
-    e2e_value = 2.0 * world * args.steps / e2e_total
-    h2d = 8 * (n + 1) + 8 * nnz + 8 * nnz + 2 * 8 * n
-    d2h = 2 * 8 * n
+        if i >= 1:
+            pin_s.append(time.perf_counter() - t0)
+    e2e_pinned = 2.0 * world * len(pin_s) / sum(pin_s)
 
     # ---- CPU baseline (rank 0, N = 1)
     cpu = None
@@ -416,7 +466,11 @@ def run_ours(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: reference generator (bit-identical to mcreach.generate_dd_matrix)",
         "config": {"workload": desc, "n": n, "nnz": nnz, "tolerance": 1e-10,
-                   "solve_pair": "jacobi + bicgstab (tree dots) from x0=0",
+                   "solve_pair": ("jacobi + bicgstab from x0=0, BiCGStab inner products in "
+                                  + {"sequential": "the reference's left-to-right order (k_xdot)",
+                                     "serial": "the reference's order (one add chain)",
+                                     "tree": "fused trees (not the reference's order)"}[args.dots]),
+                   "dots": args.dots,
                    "l2": "flushed before every step (512 MiB write); SpMV working set 144 MB",
                    "parallelism": f"replicas x{world}"},
         "time_to_solution_ms": {"jacobi": statistics.median(jac_ms),
@@ -438,11 +492,15 @@ def run_ours(args):
                                     "~52 us (profiles/r01_gather_microbench.txt)"),
                      "spmv_alone": spmv_alone},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h,
-                "note": "public API per step: DeviceMatrix upload + mcr_jacobi + mcr_bicgstab (pinned host b/x) + destroy"},
+                "d2h_bytes_per_step": d2h, "iterations": e2e_iters,
+                "note": f"drop-in per step: {via}: fresh matrix object (upload), jacobi-gpu + bicgstab-gpu, x to the host",
+                "pinned_device_api": {"value": e2e_pinned, "unit": UNIT,
+                                      "note": "DeviceMatrix from pinned arrays + mcr_jacobi + mcr_bicgstab + destroy"}},
         "gpu_launches": launches,
         "clocks": clocks.summary(),
     }
+    if other:
+        line["tree_dots"] = other
     if cpu:
         line["cpu_baseline"] = cpu
     if rank == 0:
@@ -640,6 +698,153 @@ def run_c5(args):
     return 0
 
 
+# ----------------------------------------------------------------------------- N > 1: row shards
+
+def run_sharded(args):
+    """N GPUs on ONE system: the C1/C2/C3 system's rows split contiguously over N shards
+    (the reference's _row_blocks up to +-1 row), Jacobi bit-identical to one GPU,
+    BiCGStab with rank-order inner products (the reference-order dots run on one GPU).
+    Under torchrun (WORLD_SIZE = N) one process per GPU with NCCL; otherwise one process
+    drives N shards as threads (devices from MCR_GPU_DEVICES, e.g. 0,0 puts two shards on one
+    GPU, else 0..N-1) with the in-process transport. Strong scaling: value = solves of the one
+    system per second, timed per rank with CUDA events, max over ranks."""
+    import ctypes
+
+    import numpy as np
+    import torch
+
+    from paper_1210_6412_b200 import _lib
+    from paper_1210_6412_b200.dist import Comm, ShardMatrix
+
+    world = args.gpus
+    env_world = int(os.environ.get("WORLD_SIZE", "1"))
+    torchrun = env_world > 1
+    m, b, desc, spec = make_workload(args.config)
+    n, nnz = int(m.n), int(m.m)
+    L = _lib.load()
+    if torchrun:
+        rank, local = int(os.environ["RANK"]), int(os.environ.get("LOCAL_RANK", "0"))
+        import torch.distributed as tdist
+        torch.cuda.set_device(local)
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        comms = {rank: Comm.nccl(local)}
+        devices = {rank: local}
+        ranks = [rank]
+        transport = "NCCL (one process per GPU)"
+    else:
+        tdist = None
+        env = os.environ.get("MCR_GPU_DEVICES")
+        devs = [int(d) for d in env.split(",")] if env else list(range(world))
+        if len(devs) < world:
+            raise SystemExit(f"--gpus {world} needs {world} devices (MCR_GPU_DEVICES={env})")
+        devs = devs[:world]
+        cl = Comm.local_group(world, devs)
+        comms = dict(enumerate(cl))
+        devices = dict(enumerate(devs))
+        ranks = list(range(world))
+        transport = f"in-process group on devices {devs}"
+    res = {}
+    errors = []
+
+    def run_rank(r):
+        try:
+            torch.cuda.set_device(devices[r])
+            dev = torch.device("cuda", devices[r])
+            sh = ShardMatrix.from_matrix(comms[r], m)
+            stream = torch.cuda.Stream(dev)
+            sh.set_stream(stream.cuda_stream)
+            L.mcr_set_dot_mode(sh.handle, _lib.DOTS_TREE)
+            bl = torch.from_numpy(np.ascontiguousarray(b[sh.row0:sh.row0 + sh.n])).to(dev)
+            xl = torch.empty(sh.n, dtype=torch.float64, device=dev)
+
+            def step():
+                out = []
+                for method in ("jacobi", "bicgstab"):
+                    rc, rep = sh.solve_device(method, bl.data_ptr(), None, 1e-10, 10_000, xl.data_ptr())
+                    if rc not in (_lib.MCR_OK, _lib.MCR_NOT_CONVERGED):
+                        raise RuntimeError(f"rank {r}: {method} rc={rc}: {_lib.last_error()}")
+                    out.append(rep)
+                return out
+
+            with torch.cuda.stream(stream):
+                for _ in range(args.warmup):
+                    step()
+                torch.cuda.synchronize(dev)
+                ms_, reps_ = [], None
+                for _ in range(args.steps):
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    reps_ = step()
+                    e1.record(stream)
+                    torch.cuda.synchronize(dev)
+                    ms_.append(e0.elapsed_time(e1))
+                # end to end: host slice of b in, host slice of x out, every step
+                e2e = []
+                for i in range(1 + args.steps):
+                    t0 = time.perf_counter()
+                    for method in ("jacobi", "bicgstab"):
+                        rc, _x, _rep = sh.solve(method, b[sh.row0:sh.row0 + sh.n], None, 1e-10, 10_000)
+                    if i >= 1:
+                        e2e.append(time.perf_counter() - t0)
+            res[r] = {"ms": sum(ms_), "reps": reps_, "e2e": sum(e2e), "rows": sh.n,
+                      "nnz": int(sh.info()["nnz"]), "launches": sum(int(x.kernel_launches) for x in reps_)}
+            sh.close()
+        except BaseException as e:  # noqa: BLE001
+            errors.append(e)
+
+    with ClockSampler(devices[ranks[0]]) as clocks:
+        if torchrun:
+            tdist.barrier()
+            run_rank(ranks[0])
+        else:
+            ts = [threading.Thread(target=run_rank, args=(r,)) for r in ranks]
+            for t in ts:
+                t.start()
+            for t in ts:
+                t.join()
+    for c in comms.values():
+        c.close()
+    if errors:
+        raise errors[0]
+    total_ms = max(v["ms"] for v in res.values())
+    e2e_total = max(v["e2e"] for v in res.values())
+    if torchrun:
+        t = torch.tensor([total_ms, e2e_total], dtype=torch.float64, device="cuda")
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        total_ms, e2e_total = float(t[0].item()), float(t[1].item())
+    r0 = res[ranks[0]]
+    rj, rb = r0["reps"]
+    rank0 = int(os.environ.get("RANK", "0")) if torchrun else 0
+    line = {
+        "metric": METRIC, "value": 2.0 * args.steps / (total_ms / 1e3), "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: reference generator (bit-identical to mcreach.generate_dd_matrix)",
+        "config": {"workload": desc + f", rows sharded over {world} GPU(s)", "n": n, "nnz": nnz,
+                   "tolerance": 1e-10,
+                   "solve_pair": "jacobi (bit-identical) + bicgstab (rank-order inner products) from x0=0",
+                   "l2": "inputs resident in HBM",
+                   "parallelism": f"row shards x{world}: allgather of the iterate / p / s + "
+                                  f"rank-order scalar exchange; {transport}"},
+        "iterations": {"jacobi": int(rj.iterations), "bicgstab": int(rb.iterations)},
+        "time_to_solution_ms": {"jacobi": rj.device_seconds * 1e3, "bicgstab": rb.device_seconds * 1e3},
+        "per_rank": {str(r): {"rows": v["rows"], "nnz": v["nnz"], "ms_per_step": v["ms"] / args.steps}
+                     for r, v in sorted(res.items())},
+        "e2e": {"value": 2.0 * args.steps / e2e_total, "unit": UNIT,
+                "h2d_bytes_per_step": 2 * 8 * n, "d2h_bytes_per_step": 2 * 8 * n,
+                "note": "per rank: host slice of b in, host slice of x out (mcr_jacobi / mcr_bicgstab on the shard)"},
+        "gpu_launches": r0["launches"],
+        "clocks": clocks.summary(),
+    }
+    if rank0 == 0:
+        print(json.dumps(line), flush=True)
+    if tdist:
+        tdist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -653,11 +858,20 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--storage", default="auto", choices=sorted(STORAGES),
                     help="C5 layout: auto (band-staged at this size), tiles or staged")
+    ap.add_argument("--dots", default="sequential", choices=["sequential", "tree", "serial"],
+                    help="BiCGStab inner products: the reference's order (default) or fused trees")
     args = ap.parse_args()
+    env_world = int(os.environ.get("WORLD_SIZE", "1"))
+    if env_world > 1 and env_world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={env_world}")
     if args.impl == "reference":
         return run_reference_arm(args)
     if args.config == "c5":
+        if args.gpus > 1 and env_world == 1:
+            raise SystemExit("--config c5 at --gpus > 1 runs under torchrun (one process per GPU)")
         return run_c5(args)
+    if args.gpus > 1:
+        return run_sharded(args)
     return run_ours(args)
 
 

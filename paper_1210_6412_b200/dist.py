@@ -241,6 +241,24 @@ def bicgstab_solve_sharded(shard: ShardMatrix, b_local, config: Optional[SolverC
     return _solve_sharded("bicgstab", shard, b_local, config)[0]
 
 
+def check_csr(m) -> None:
+    """The CsrMatrix invariants the upload enforces (sparse.py:101-118: row starts from 0 to
+    nnz, non-decreasing; columns in range and strictly ascending within each row), checked on
+    the host before any rank starts, so a malformed matrix fails at once on every rank instead
+    of leaving the other ranks waiting at the first exchange."""
+    n = int(m.n)
+    rs = np.asarray(m.rstart, dtype=np.int64)
+    col = np.asarray(m.col, dtype=np.int64)
+    if rs.shape != (n + 1,) or rs[0] != 0 or rs[-1] != col.shape[0] or np.any(np.diff(rs) < 0):
+        raise DimensionMismatch("malformed CSR row starts")
+    if col.size and (col.min() < 0 or col.max() >= n):
+        raise DimensionMismatch("CSR column index out of range")
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(rs))
+    same = rows[1:] == rows[:-1]
+    if np.any(np.diff(col)[same] <= 0):
+        raise DimensionMismatch("CSR columns not strictly ascending within a row")
+
+
 def solve_local_group(method: str, m, b, world: int, config: Optional[SolverConfig] = None,
                       devices: Optional[Sequence[int]] = None, p2p: bool = False):
     """Solve ``m x = b`` as ``world`` row shards driven by ``world`` threads of this process.
@@ -254,6 +272,7 @@ def solve_local_group(method: str, m, b, world: int, config: Optional[SolverConf
         raise DimensionMismatch(f"right-hand side of shape {b.shape} against dimension {m.n}")
     if m.n < 1 or shard_rows(int(m.n), world, world - 1)[1] < 1:
         raise ValueError(f"{world} ranks need every rank to hold rows (n = {m.n})")
+    check_csr(m)
     comms = Comm.local_group(world, devices)
     shards = [None] * world
     out = [None] * world

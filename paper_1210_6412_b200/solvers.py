@@ -74,10 +74,16 @@ class Breakdown(SolverError):
 class SolverConfig:
     """solvers.py:81-109, plus two GPU fields.
 
-    ``device``: CUDA ordinal of the solve. ``dot_products``: ``"tree"`` (default) reduces
-    BiCGStab's inner products with deterministic fixed-shape trees fused into the producing
-    kernels; ``"sequential"`` reproduces the reference's strictly left-to-right
-    ``_dot_ascending`` (solvers.py:136-141) bit for bit, at one dependent add per element.
+    ``device``: CUDA ordinal of the solve. ``dot_products``: how BiCGStab's inner products
+    are summed. ``"sequential"`` (default) is the reference's own left-to-right order
+    (``_dot_ascending``, solvers.py:136-141), bit for bit, computed in parallel by k_xdot
+    (csrc/xdot.cuh), so x, the iteration count, the residual and breakdowns equal the
+    reference's; with ``parallel_dot_products`` the row-sharded solvers sum per
+    ``_row_blocks`` block and add the block results in order, as ``_ParOps.dot``
+    (solvers.py:384-396). ``"tree"`` is the fastest mode: deterministic fixed-shape trees
+    fused into the producing kernels -- not the reference's order, so the stopping iteration
+    can differ (C2: 82 vs the reference's 79). ``"serial"`` gives the sequential bits from a
+    single dependent add chain (a slow cross-check of k_xdot).
     """
 
     tolerance: float = 1e-10
@@ -86,7 +92,7 @@ class SolverConfig:
     workers: Optional[int] = None
     parallel_dot_products: bool = False
     device: int = 0
-    dot_products: str = "tree"
+    dot_products: str = "sequential"
 
     def __post_init__(self):
         if not self.tolerance > 0.0:
@@ -95,8 +101,8 @@ class SolverConfig:
             raise ValueError("max_iterations must be at least 1")
         if self.workers is not None and self.workers < 1:
             raise ValueError("workers must be at least 1")
-        if self.dot_products not in ("tree", "sequential"):
-            raise ValueError("dot_products must be 'tree' or 'sequential'")
+        if self.dot_products not in ("sequential", "tree", "serial"):
+            raise ValueError("dot_products must be 'sequential', 'tree' or 'serial'")
 
     def resolved_workers(self) -> int:
         return self.workers if self.workers is not None else (os.cpu_count() or 1)
@@ -274,7 +280,7 @@ def _empty_result(start: float) -> SolveResult:
 
 
 def _solve(method: str, m, b, config, dots: Optional[str] = None,
-           device: Optional[int] = None) -> SolveResult:
+           device: Optional[int] = None, dot_blocks: int = 1) -> SolveResult:
     cfg = config or SolverConfig()
     b = _check_system(m, b)
     start = time.perf_counter()
@@ -284,7 +290,7 @@ def _solve(method: str, m, b, config, dots: Optional[str] = None,
     x0 = _initial_guess(m.n, cfg)
     with dm.lock:
         rc, x, rep = dm.solve(method, b, x0, cfg.tolerance, cfg.max_iterations,
-                              dots or getattr(cfg, "dot_products", "tree"))
+                              dots or getattr(cfg, "dot_products", "sequential"), dot_blocks)
     return finish(rc, x, rep, start)
 
 
@@ -387,9 +393,13 @@ def _solve_parallel(method: str, m, b, config) -> SolveResult:
     start = time.perf_counter()
     if m.n == 0:
         return _empty_result(start)
-    if getattr(cfg, "dot_products", "tree") == "sequential":
-        # the reference's sequential dots are one chain over all rows: one GPU
-        return _solve(method, m, b, cfg, dots="sequential")
+    dots = getattr(cfg, "dot_products", "sequential")
+    if method == "bicgstab" and dots != "tree":
+        # the reference's inner products (solvers.py:384-396): one left-to-right chain over
+        # all rows, or with parallel_dot_products one chain per _row_blocks block of
+        # resolved_workers() blocks, block results added in order -- on one GPU
+        blocks = cfg.resolved_workers() if getattr(cfg, "parallel_dot_products", False) else 1
+        return _solve(method, m, b, cfg, dots=dots, dot_blocks=max(1, int(blocks)))
     devices = parallel_devices(int(m.n), cfg)
     from .dist import shard_rows, solve_local_group
     while len(devices) > 1 and shard_rows(int(m.n), len(devices), len(devices) - 1)[1] < 1:
@@ -410,9 +420,12 @@ def jacobi_solve_parallel(m, b, config: Optional[SolverConfig] = None) -> SolveR
 
 
 def bicgstab_solve_parallel(m, b, config: Optional[SolverConfig] = None) -> SolveResult:
-    """Row-sharded BiCGStab over ``config.workers`` GPUs (solvers.py:429-447): p and s
-    exchanged before each product, every inner product reduced per shard and then summed in
-    ascending shard order, identically on all shards."""
+    """solvers.py:429-447. With the reference's dots (default) the result is the reference's
+    ``bicgstab_solve_parallel`` bit for bit -- sequential inner products, or per-block ones
+    when ``parallel_dot_products`` is set (blocks = ``resolved_workers()``, as the reference)
+    -- computed on one GPU. With ``dot_products="tree"`` the rows shard over
+    ``config.workers`` GPUs: p and s exchanged before each product, every inner product
+    reduced per shard and summed in ascending shard order, identically on all shards."""
     return _solve_parallel("bicgstab", m, b, config)
 
 

@@ -29,3 +29,26 @@ def test_algorithmic_bytes():
     assert ab["spmv"] == 12 * 10 ** 7 + 8 * (10 ** 6 + 1) + 16 * 10 ** 6
     assert ab["jacobi_sweep"] == 12 * 9 * 10 ** 6 + 8 * (10 ** 6 + 1) + 32 * 10 ** 6
     assert ab["bicgstab_iteration"] == 2 * (12 * 10 ** 7 + 8 * (10 ** 6 + 1)) + 152 * 10 ** 6
+
+
+def test_gpus_flag_is_honoured(monkeypatch):
+    """--gpus N > 1 runs the row-sharded workload (run_sharded, n_gpus = N) rather than a
+    single GPU; a WORLD_SIZE that disagrees with --gpus is an error."""
+    sys.path.insert(0, ROOT)
+    import bench
+    seen = {}
+    monkeypatch.setattr(bench, "run_sharded", lambda args: seen.setdefault("sharded", args.gpus) and 0)
+    monkeypatch.setattr(bench, "run_ours", lambda args: seen.setdefault("single", args.gpus) and 0)
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "2", "--steps", "1", "--warmup", "0"])
+    bench.main()
+    assert seen == {"sharded": 2}
+    seen.clear()
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--steps", "1", "--warmup", "0"])
+    bench.main()
+    assert seen == {"single": 1}
+    monkeypatch.setenv("WORLD_SIZE", "4")
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "2"])
+    import pytest
+    with pytest.raises(SystemExit):
+        bench.main()

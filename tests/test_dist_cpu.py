@@ -206,3 +206,21 @@ def test_registry_parallel_device_choice(monkeypatch):
     import pytest
     with pytest.raises(ValueError):
         gs.parallel_devices(10, gs.SolverConfig())
+
+
+def test_malformed_csr_rejected_before_ranks_start():
+    """solve_local_group validates the CSR once on the host (no rank can fail alone and leave
+    the others waiting at an exchange)."""
+    import numpy as np
+    import pytest
+    from paper_1210_6412_b200 import dist
+    from paper_1210_6412_b200.sparse import CsrMatrix, DimensionMismatch
+    rs = np.array([0, 2, 3], dtype=np.int64)
+    good = CsrMatrix(2, rs, np.array([0, 1, 1]), np.array([1.0, 2.0, 3.0]))
+    dist.check_csr(good)
+    for col in ([1, 0, 1], [0, 0, 1], [0, 2, 1]):
+        with pytest.raises(DimensionMismatch):
+            dist.check_csr(CsrMatrix(2, rs, np.array(col), np.array([1.0, 2.0, 3.0])))
+    with pytest.raises(DimensionMismatch):
+        dist.solve_local_group("jacobi", CsrMatrix(2, rs, np.array([1, 0, 1]),
+                                                   np.array([1.0, 2.0, 3.0])), np.ones(2), 2)

@@ -53,10 +53,10 @@ def test_bench_csv_rows_for_gpu_methods(tmp_path, capsys):
     from paper_1210_6412_b200.__main__ import main
     out = tmp_path / "t1.csv"
     code, _, err = run(capsys, main, "bench", "--table1", "--trials", "1", "--methods",
-                       "jacobi-seq,jacobi-gpu,bicgstab-gpu", "--output", out)
+                       "jacobi-seq,jacobi-gpu,bicgstab-seq,bicgstab-gpu", "--output", out)
     assert code == 0, err
     rows = list(csv.DictReader(open(out)))
-    assert len(rows) == 18 * 3
+    assert len(rows) == 18 * 4
     by = {}
     for r in rows:
         by.setdefault((r["n"], r["m"]), {})[r["method"]] = r
@@ -65,6 +65,8 @@ def test_bench_csv_rows_for_gpu_methods(tmp_path, capsys):
         assert cell["jacobi-gpu"]["iterations"] == cell["jacobi-seq"]["iterations"]
         assert cell["jacobi-gpu"]["converged"].lower() == "true"
         assert cell["bicgstab-gpu"]["converged"].lower() == "true"
+        # BiCGStab too: the GPU sums its inner products in the reference's order
+        assert cell["bicgstab-gpu"]["iterations"] == cell["bicgstab-seq"]["iterations"]
 
 
 def test_unknown_method_still_rejected(tmp_path, capsys):

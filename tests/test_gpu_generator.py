@@ -72,9 +72,9 @@ def test_generated_system_solves_like_oracle(mods):
     assert np.array_equal(x, oj["x"])
     assert float(rep.residual_inf).hex() == float(oj["residual_inf"]).hex()
     rc, xb, repb = dm.solve("bicgstab", b, None, 1e-10, 10_000)
-    ob = oracle.bicgstab(ref, b)
-    assert rc == 0 and abs(repb.iterations - ob["iterations"]) <= 6
-    assert np.max(np.abs(xb - ob["x"])) / max(1.0, np.max(np.abs(ob["x"]))) <= 1e-9
+    ob = oracle.bicgstab(ref, b)  # the reference's algorithm incl. its left-to-right dots
+    assert rc == 0 and repb.iterations == ob["iterations"]
+    assert np.array_equal(xb, ob["x"])
 
 
 def test_sharded_generated_solve_bit_identical(mods):
