@@ -5,9 +5,10 @@
 order, a float64 vector, ``(MarkovChain, GoalSet)`` validated like ``validate()`` -- parsed by
 the multithreaded C++ readers in ``libmcr.so`` (``csrc/formats.cpp``). A file outside their
 well-formed plain-decimal subset (any error, duplicate, failed check, ``inf``/``nan``,
-underscores, non-ASCII) is handed to the reference's own reader when ``mcreach`` is importable,
-so errors (``ParseError`` with its line number, ``RowSumError``, ...) are exactly the
-reference's; without ``mcreach`` a ``ParseError`` mirror carrying the reader's reason is raised.
+underscores, non-ASCII) goes to this package's line-by-line readers (``textio.py``), which
+restate the reference's rules, so results and errors (``ParseError`` with its line number,
+``RowSumError``, ``DuplicateEntry``, ...) are the reference's -- its own classes when
+``mcreach`` is importable. The reference's code is never run.
 """
 
 from __future__ import annotations
@@ -18,26 +19,13 @@ from typing import Optional
 
 import numpy as np
 
-from . import _lib
+from . import _lib, textio
 from .sparse import CsrMatrix
 
 __all__ = ["ParseError", "read_matrix", "read_vector", "read_dtmc"]
 
 
-class ParseError(ValueError):
-    """formats.py:51-56 (the reference's class is used when mcreach is importable)."""
-
-    def __init__(self, message: str, line: Optional[int] = None):
-        self.line = line
-        super().__init__(f"line {line}: {message}" if line else message)
-
-
-def _reference_formats():
-    try:
-        import mcreach.formats as mf
-        return mf
-    except Exception:
-        return None
+ParseError = textio.ParseError  # formats.py:51-56 (the reference's class is raised when importable)
 
 
 def _read(fn_name: str, path):
@@ -49,13 +37,6 @@ def _read(fn_name: str, path):
     if rc == _lib.MCR_UNSUPPORTED_INPUT:
         return L, None, L.mcr_text_reason().decode(errors="replace")
     raise _lib.NativeLibraryError(f"{fn_name} failed with status {rc}")
-
-
-def _defer(name: str, path, reason: str):
-    mf = _reference_formats()
-    if mf is not None:
-        return getattr(mf, name)(path)  # the reference's result or its exact error
-    raise ParseError(reason)
 
 
 def _info(L, h):
@@ -84,7 +65,7 @@ def read_matrix(path):
     """formats.py:89-113."""
     L, h, why = _read("mcr_read_matrix", path)
     if h is None:
-        return _defer("read_matrix", path, why)
+        return textio.read_matrix(path, _matrix_type())
     try:
         n, m, _, _ = _info(L, h)
         rs, col, val = _csr(L, h, n, m)
@@ -97,7 +78,7 @@ def read_vector(path) -> np.ndarray:
     """formats.py:128-145."""
     L, h, why = _read("mcr_read_vector", path)
     if h is None:
-        return _defer("read_vector", path, why)
+        return textio.read_vector(path)
     try:
         n, _, _, _ = _info(L, h)
         v = np.empty(n, dtype=np.float64)
@@ -111,7 +92,8 @@ def read_dtmc(path):
     """formats.py:160-230: (MarkovChain, GoalSet), reference types when importable."""
     L, h, why = _read("mcr_read_dtmc", path)
     if h is None:
-        return _defer("read_dtmc", path, why)
+        n, initial, goals, p = textio.read_dtmc_parts(path)
+        return _chain(n, p.rstart, p.col, p.nonzero, initial, np.array(goals, dtype=np.int64))
     try:
         n, m, initial, ng = _info(L, h)
         rs, col, val = _csr(L, h, n, m)
@@ -119,6 +101,10 @@ def read_dtmc(path):
         L.mcr_text_export(h, None, None, None, goals.ctypes.data)
     finally:
         L.mcr_text_destroy(h)
+    return _chain(n, rs, col, val, initial, goals)
+
+
+def _chain(n, rs, col, val, initial, goals):
     try:
         from mcreach.markov import GoalSet, MarkovChain
         return MarkovChain(n=n, transitions=_matrix_type()(n, rs, col, val), initial=initial), \

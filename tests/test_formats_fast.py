@@ -2,7 +2,9 @@
 against the reference's file semantics (mcreach/formats.py:89-232): values bit-identical to
 Python's float() (17-digit round trips), csr_from_triplets order with zeros dropped, comments,
 blank lines, CRLF, keyword lines anywhere in chain files; every malformed / non-plain file is
-refused by the fast path (MCR_UNSUPPORTED_INPUT) and deferred to the reference reader."""
+refused by the fast path (MCR_UNSUPPORTED_INPUT) and read by the package's own line-by-line
+readers (textio.py), whose results and errors are compared here with the reference reader's
+(the reference is the checker only; the package never calls it)."""
 
 import ctypes
 import os
@@ -171,7 +173,7 @@ def test_dtmc_outside_fast_subset_is_deferred(tmp_path, body):
     assert rc_of("mcr_read_dtmc", p) == _lib.MCR_UNSUPPORTED_INPUT
 
 
-def test_deferred_errors_are_the_references(tmp_path):
+def test_errors_are_the_references(tmp_path):
     mf = pytest.importorskip("mcreach.formats")
     p = tmp_path / "c.dtmc"
     p.write_text("dtmc\nstates 2\ninitial 0\ngoal 1\n0 1 0.5\n0 1 0.5\n1 1 1\n")
@@ -190,3 +192,111 @@ def test_against_reference_reader(tmp_path):
     a, r = formats.read_matrix(p), mf.read_matrix(p)
     assert np.array_equal(a.rstart, r.rstart) and np.array_equal(a.col, r.col)
     assert np.array_equal(a.nonzero, r.nonzero)
+
+
+MATRIX_BODIES = [
+    "matrix 2 1\n0 1 1_0.5\n",
+    "matrix 2 1\n0 1 inf\n",
+    "matrix 2 1\n0 1 nan\n",
+    "matrix 2 2\n0 1 0.5\n0 1 0.5\n",
+    "matrx 2 2\n",
+    "matrix 2 3\n0 1 0.5\n",
+    "matrix 2 1\n0 x 0.5\n",
+    "matrix 2 1\n0 1 0.5 7\n",
+    "matrix 2 1\n0 5 0.5\n",
+    "matrix -1 0\n",
+    "matrix 2 1\r0 1 0.5\n",
+    "matrix 3 2\n0 1 1e400\n2 2 -0\n",
+    "",
+    "# only a comment\n",
+]
+VECTOR_BODIES = ["vector 2\n1.5\n", "vector 1\n1 2\n", "vectr 1\n1\n", "vector 2\n1\ninf\n", ""]
+DTMC_BODIES = [
+    "dtmc\nstates 2\ngoal 1\n0 1 1\n1 1 1\n",
+    "states 2\n",
+    "dtmc\nstates 2\ninitial 0\ngoal 1\n0 1 0.5\n0 1 0.5\n1 1 1\n",
+    "dtmc\nstates 2\ninitial 0\ngoal 1\n0 1 0.9\n1 1 1\n",
+    "dtmc\nstates 2\ninitial 0\ngoal 5\n0 1 1\n1 1 1\n",
+    "dtmc\nstates 2\nstates 2\ninitial 0\ngoal 1\n0 1 1\n1 1 1\n",
+    "dtmc\nstates 2\ninitial 0\ngoal 1\n0 1 1.5\n1 1 1\n",
+    "dtmc\nstates 2\ninitial 7\ngoal 1\n0 1 1\n1 1 1\n",
+    "dtmc\nstates 2\ninitial 0\ngoal 1\n0 3 1\n1 1 1\n",
+    "dtmc\nstates 2\ninitial 0\ngoal\n0 1 1\n1 1 1\n",
+    "dtmc\nstates 2\ninitial 0\ngoal 1\n0 1 0.5 9\n1 1 1\n",
+    "dtmc\nstates 0\ninitial 0\ngoal 0\n",
+    "dtmc\nstates 3\ninitial 0\ngoal 2\n0 1 0.25\n0 2 0.75\n1 1 1\n2 2 1_0e-1\n",
+    "dtmc\nstates 2\ninitial 0\ngoal 1\n0 1 -0.5\n0 0 1.5\n1 1 1\n",
+    "",
+]
+
+
+def _outcome(fn, path):
+    try:
+        r = fn(path)
+    except Exception as err:  # noqa: BLE001
+        return ("error", type(err).__name__, str(err), getattr(err, "line", None))
+    if isinstance(r, tuple):
+        chain, goals = r
+        t = chain.transitions
+        return ("ok", t.rstart.tolist(), t.col.tolist(), np.asarray(t.nonzero).tobytes(),
+                chain.initial, sorted(getattr(goals, "members", goals)))
+    if hasattr(r, "rstart"):
+        return ("ok", r.rstart.tolist(), r.col.tolist(), np.asarray(r.nonzero).tobytes())
+    return ("ok", np.asarray(r, dtype=np.float64).tobytes())
+
+
+@pytest.mark.parametrize("kind,body", [("matrix", b) for b in MATRIX_BODIES]
+                         + [("vector", b) for b in VECTOR_BODIES]
+                         + [("dtmc", b) for b in DTMC_BODIES])
+def test_outside_fast_subset_same_as_reference(tmp_path, kind, body):
+    """Files the C++ readers refuse: the package's own readers give the reference reader's
+    result or its exact error (class, message, line number)."""
+    mf = pytest.importorskip("mcreach.formats")
+    p = tmp_path / f"f.{kind}"
+    p.write_bytes(body.encode())
+    ours = _outcome(getattr(formats, f"read_{kind}"), p)
+    ref = _outcome(getattr(mf, f"read_{kind}"), p)
+    assert ours == ref, (body, ours, ref)
+    if ours[0] == "error":  # the reference's own exception classes
+        try:
+            getattr(formats, f"read_{kind}")(p)
+        except Exception as err:  # noqa: BLE001
+            assert type(err).__module__.startswith("mcreach"), type(err)
+
+
+def test_mirrors_without_the_reference(tmp_path, monkeypatch):
+    """Without mcreach importable the mirrors carry the same messages and fields."""
+    from paper_1210_6412_b200 import textio
+    monkeypatch.setattr(textio, "_ref", lambda module: None)
+    p = tmp_path / "c.dtmc"
+    p.write_text("dtmc\nstates 2\ninitial 0\ngoal 1\n0 1 0.5\n0 1 0.5\n1 1 1\n")
+    with pytest.raises(textio.ParseError) as err:
+        textio.read_dtmc_parts(p)
+    assert err.value.line == 6 and "duplicate transition 0 -> 1 (first on line 5)" in str(err.value)
+    p.write_text("dtmc\nstates 2\ninitial 0\ngoal 1\n0 1 0.9\n1 1 1\n")
+    with pytest.raises(textio.RowSumError) as err:
+        textio.read_dtmc_parts(p)
+    assert err.value.state == 0 and str(err.value) == "row 0 sums to 0.9, expected 1"
+    p.write_text("matrix 2 2\n0 1 0.5\n0 1 0.25\n")
+    from paper_1210_6412_b200.sparse import DuplicateEntry
+    with pytest.raises(DuplicateEntry):
+        textio.read_matrix(p)
+
+
+def test_row_sums_left_to_right():
+    """validate's row sums add each row's entries in column order from 0.0 (scipy's
+    csr_matvec with a vector of ones), not pairwise."""
+    from paper_1210_6412_b200 import textio
+    from paper_1210_6412_b200.sparse import csr_from_triplets
+    rng = np.random.default_rng(3)
+    for _ in range(20):
+        n = int(rng.integers(1, 40))
+        ent = [(i, j, float(rng.uniform(0, 1))) for i in range(n) for j in range(n) if rng.random() < 0.5]
+        p = csr_from_triplets(n, ent)
+        want = np.zeros(n)
+        for i in range(n):
+            acc = 0.0
+            for k in range(p.rstart[i], p.rstart[i + 1]):
+                acc = acc + float(p.nonzero[k])
+            want[i] = acc
+        assert np.array_equal(textio.row_sums(p), want)
