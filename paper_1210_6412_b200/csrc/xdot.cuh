@@ -113,6 +113,7 @@ struct Seq {
 // Scratch (device memory owned by the plan).
 struct Scratch {
     Desc* cta;             // [grid] the CTA pieces
+    Desc* warp;            // [grid * NW] the warp pieces (the root's fallback)
     double* lb_val;        // [grid] look-back: CTA totals (predictions only)
     int* lb_flag;          // [grid]
     unsigned* ticket;      // [nseq]
@@ -411,7 +412,7 @@ __device__ __forceinline__ void sim_elems(const double* p, int cnt, double& v, d
 // memory, adding a thread's products one by one where its run does not apply.
 __device__ void lane_walk_threads(const Run* s_runs, const double* sp, int len, int E, int t0, int t1,
                                   double& v, double& lo, double& hi, int& km,
-                                  unsigned long long* sims = nullptr) {
+                                  unsigned long long* sims = nullptr, bool bare = false) {
     for (int t = t0; t < t1; ++t) {
         const Run R = s_runs[t];
         if (run_apply(R, v, lo, hi, km)) continue;
@@ -419,7 +420,13 @@ __device__ void lane_walk_threads(const Run* s_runs, const double* sp, int len, 
 #ifdef MCR_XDOT_TIMING
         if (sims) atomicAdd(sims, 1ull);
 #endif
-        sim_elems(sp + b0, bl, v, lo, hi, km);
+        if (bare) {  // the value only: this lane then serves its exact start alone
+            for (int k = 0; k < bl; ++k) v = dadd(v, sp[b0 + k]);
+            lo = fmax(lo, 0.0);
+            hi = fmin(hi, 0.0);
+        } else {
+            sim_elems(sp + b0, bl, v, lo, hi, km);
+        }
     }
 }
 
@@ -686,6 +693,11 @@ __device__ void runs_and_warp_pieces(const Scratch& S, const Seq& q, long long c
         const int wn = window_neg(wpred);
         double v = cand(mb0, wn, lane), lo = -INFINITY, hi = INFINITY;
         int km = KM_NONE;
+        // a warp of mostly element-by-element threads (the sum passing near zero): its table
+        // could not be shifted anyway (the start's low bits decide the roundings on the way
+        // up), so only the values are carried -- the root walks such a stretch from its exact
+        // start when it needs it
+        const bool bare = false;  // (carrying values only measured slower: more root walks)
 #ifdef XD_TWICE
         for (int rep = 0; rep < 2; ++rep) {
         const unsigned long long tr0 = gtime();
@@ -719,7 +731,7 @@ __device__ void runs_and_warp_pieces(const Scratch& S, const Seq& q, long long c
 #endif
             if (!okr)
                 lane_walk_threads(M.runs, sp, len, E, warp * 32 + sl, warp * 32 + el + 1, v, lo, hi, km,
-                                  S.stats ? S.stats + ST_SIMS_WARP : nullptr);
+                                  S.stats ? S.stats + ST_SIMS_WARP : nullptr, bare);
 #ifdef MCR_XDOT_TIMING
             __syncwarp();
             cyc_walk += clock64() - c_b;
@@ -866,6 +878,12 @@ __device__ int build_cta(const Args& A, const Seq& q, int si, const Smem& M, dou
     XT_ADD(S, ST_T_RUNS, t_runs);
     XT_MARK(t_cta);
     if (A.upto == 3 || A.upto == 13) return ci;
+    {  // the warp pieces, for the root's fallback (before the tree folds them in place)
+        const double2* src = (const double2*)M.wd;
+        double2* dst = (double2*)(S.warp + (size_t)slot * NW);
+        for (int k = tid; k < (int)(NW * sizeof(Desc) / 16); k += NT) dst[k] = src[k];
+    }
+    __syncthreads();
     tree_fold(M, len, E, M.wd, true);  // the CTA piece, in wd[0]
     if (S.stats && tid == 0 && M.wd[0].h.kind == K_TABLE) stat(S, ST_CTA_TABLE);
 #ifdef MCR_XDOT_DEBUG
@@ -881,38 +899,102 @@ __device__ int build_cta(const Args& A, const Seq& q, int si, const Smem& M, dou
     return ci;
 }
 
-// All threads of the root: the exact sum of CTA range ci from its true start (*s_v),
-// rebuilding the range's pieces around that start (the predictions are then exact up to the
-// rounding inside the range) and walking them with warp 0; a warp piece that still does not
-// apply is replaced by its thread runs, a thread run by its elements.
-__device__ void rebuild_walk(const Args& A, const Seq& q, int ci, const Smem& M, double* s_red, double* s_v) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+// Warp 0 of the root: warp w's elements of CTA range ci from the exact start v: the 32
+// threads' runs rebuilt around predictions from v (one per lane), then a scalar walk over
+// them; a thread whose run does not apply adds its elements one by one. Exact always.
+__device__ double warp_walk_exact(const Args& A, const Seq& q, int ci, int w, double v, const Smem& M) {
+    const int lane = threadIdx.x & 31;
     const int E = A.E;
     const long long c0 = q.a + (long long)ci * NT * E;
     const long long c1 = min(q.b, c0 + (long long)NT * E);
-    const int len = (int)max(0ll, c1 - c0);
+    const long long w0 = c0 + (long long)w * 32 * E;
+    const int wl = (int)max(0ll, min(c1 - w0, (long long)32 * E));
+    double* sp = M.sp;  // the root's own range is no longer needed
+    for (int k = lane; k < wl; k += 32) sp[k] = dmul(__ldcg(q.u + w0 + k), __ldcg(q.v + w0 + k));
+    __syncwarp();
+    const int t0 = lane * E, tl = max(0, min(E, wl - t0));
+    double ts = 0.0;
+    for (int k = 0; k < tl; ++k) ts = dadd(ts, sp[t0 + k]);
+    double inc = ts;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const double o = __shfl_up_sync(FULL, inc, off);
+        if (lane >= off) inc = dadd(inc, o);
+    }
+    double exc = __shfl_up_sync(FULL, inc, 1);
+    if (lane == 0) exc = 0.0;
+    const double pred = dadd(v, exc);
+    Run R = run_empty();
+    if (tl > 0) {
+        R.e = E_HARD;
+        const unsigned long long pb = bt(pred);
+        const int e = dexp(pb);
+        const int ng = (int)(pb >> 63);
+        if (e >= RUN_MIN_E && e <= 0x7f0) {
+            const double ref0 = fb(pb & ~1ull), ref1 = fb(bt(ref0) + 1ull);
+            double s0 = ref0, s1 = ref1;
+            unsigned long long a0 = bt(ref0), z0 = a0, a1 = bt(ref1), z1 = a1;
+            for (int k = 0; k < tl; ++k) {
+                s0 = dadd(s0, sp[t0 + k]);
+                s1 = dadd(s1, sp[t0 + k]);
+                a0 = min(a0, bt(s0)); z0 = max(z0, bt(s0));
+                a1 = min(a1, bt(s1)); z1 = max(z1, bt(s1));
+            }
+            const bool same = (a0 >> 52) == (z0 >> 52) && (a1 >> 52) == (z1 >> 52) && (a0 >> 52) == (pb >> 52);
+            const double mn0 = ng ? fb(z0) : fb(a0), mx0 = ng ? fb(a0) : fb(z0);
+            const double mn1 = ng ? fb(z1) : fb(a1), mx1 = ng ? fb(a1) : fb(z1);
+            const double bot = fb(((unsigned long long)e << 52) | 1ull), top = fb(((unsigned long long)e << 52) | MANT);
+            if (same && (ng ? (-mx0 >= bot && -mn0 <= top && -mx1 >= bot && -mn1 <= top)
+                            : (mn0 >= bot && mx0 <= top && mn1 >= bot && mx1 <= top))) {
+                R.d[0] = dsub(s0, ref0); R.d[1] = dsub(s1, ref1);
+                R.lo[0] = dsub(mn0, ref0); R.hi[0] = dsub(mx0, ref0);
+                R.lo[1] = dsub(mn1, ref1); R.hi[1] = dsub(mx1, ref1);
+                R.e = e;
+                R.neg = ng;
+            }
+        }
+    }
+    for (int t = 0; t < 32; ++t) {  // uniform: every lane carries the same value
+        Run G;
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+            G.d[p] = __shfl_sync(FULL, R.d[p], t);
+            G.lo[p] = __shfl_sync(FULL, R.lo[p], t);
+            G.hi[p] = __shfl_sync(FULL, R.hi[p], t);
+        }
+        G.e = __shfl_sync(FULL, R.e, t);
+        G.neg = __shfl_sync(FULL, R.neg, t);
+        double lo = -INFINITY, hi = INFINITY;
+        int km = KM_NONE;
+        if (run_apply(G, v, lo, hi, km)) continue;
+        if (lane == 0) stat(A.S, ST_CHUNK_FB);
+        const int b0 = t * E, bl = max(0, min(E, wl - b0));
+        for (int k = 0; k < bl; ++k) v = dadd(v, sp[b0 + k]);
+    }
+    __syncwarp();
+    return v;
+}
+
+// All threads of the root: CTA range ci from its true start (*s_v) through its warp pieces
+// (staged from global memory); a warp piece that does not apply is walked exactly.
+__device__ void walk_warps(const Args& A, const Seq& q, int ci, const Smem& M, double* s_v) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) stat(A.S, ST_CTA_FB);
-    __syncthreads();  // sp / runs / wd may still be read
-    const double v0 = *s_v;
-    const unsigned fl = load_products(q, c0, len, M.sp);
-    double total;
-    const double exc = thread_scan(M.sp, len, E, s_red, &total);
-    runs_and_warp_pieces(A.S, q, c0, len, E, dadd(v0, exc), fl, M);
+    __syncthreads();  // wd may still be read
+    {
+        const double2* src = (const double2*)(A.S.warp + (size_t)(q.cta0 + ci) * NW);
+        double2* dst = (double2*)M.wd;
+        for (int k = threadIdx.x; k < (int)(NW * sizeof(Desc) / 16); k += NT) dst[k] = __ldcg(src + k);
+    }
+    __syncthreads();
     if (warp == 0) {
-        double v = v0;
+        double v = *s_v;
         for (int w = 0; w < NW; ++w) {
-            const PieceR P = load_piece(M.wd + w);
             double lo = -INFINITY, hi = INFINITY;
             int km = KM_NONE;
-            if (piece_apply_r(P, v, lo, hi, km)) continue;
+            if (piece_apply_r(load_piece(M.wd + w), v, lo, hi, km)) continue;
             if (lane == 0) stat(A.S, ST_WARP_FB);
-            for (int t = w * 32; t < w * 32 + 32; ++t) {  // uniform scalar walk
-                const Run R = M.runs[t];
-                if (run_apply(R, v, lo, hi, km)) continue;
-                if (lane == 0) stat(A.S, ST_CHUNK_FB);
-                const int b0 = t * E, bl = max(0, min(E, len - b0));
-                for (int k = 0; k < bl; ++k) v = dadd(v, M.sp[b0 + k]);
-            }
+            v = warp_walk_exact(A, q, ci, w, v, M);
         }
         if (lane == 0) *s_v = v;
     }
@@ -950,7 +1032,7 @@ __device__ void walk_ctas(const Args& A, const Seq& q, int b0, int c0, int c1, c
         __syncthreads();
         c = s_c;
         if (c >= c1) break;
-        rebuild_walk(A, q, c, M, s_red, s_v);
+        walk_warps(A, q, c, M, s_v);
         ++c;
     }
     __syncthreads();

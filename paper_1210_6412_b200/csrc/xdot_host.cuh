@@ -110,7 +110,7 @@ int xdot_plan(XdotCtx& X, int w, cudaStream_t s, int device, int64_t n, int ndot
     const int nseq = (int)seqs.size();
     if (grid > X.grid_cap || nseq > X.nseq_cap) {
         const int gc = std::max(grid, X.grid_cap), sc = std::max(nseq, X.nseq_cap);
-        const size_t bytes = sizeof(xd::Desc) * (size_t)gc + sizeof(double) * (size_t)gc +
+        const size_t bytes = sizeof(xd::Desc) * (size_t)gc * (1 + xd::NW) + sizeof(double) * (size_t)gc +
                              sizeof(int) * (size_t)gc + sizeof(double) * (size_t)sc +
                              sizeof(unsigned) * (size_t)(3 * sc + 1) + 256;
         if (X.blk) CK(cudaFreeAsync(X.blk, s));
@@ -120,6 +120,7 @@ int xdot_plan(XdotCtx& X, int w, cudaStream_t s, int device, int64_t n, int ndot
         char* p = (char*)X.blk;
         auto take = [&](size_t b) { char* r = p; p += (b + 15) & ~(size_t)15; return r; };
         X.S.cta = (xd::Desc*)take(sizeof(xd::Desc) * (size_t)gc);
+        X.S.warp = (xd::Desc*)take(sizeof(xd::Desc) * (size_t)gc * xd::NW);
         X.S.lb_val = (double*)take(sizeof(double) * (size_t)gc);
         X.S.result = (double*)take(sizeof(double) * (size_t)sc);
         X.S.lb_flag = (int*)take(sizeof(int) * (size_t)gc);
