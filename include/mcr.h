@@ -142,6 +142,11 @@ MCR_API int mcr_xdot(int device, int64_t n, const double* u, const double* v, in
 MCR_API int mcr_xdot_bench(int device, int64_t n, const double* u, const double* v, int nblocks,
                            int reps, double* out, double* ms, uint64_t* stats);
 
+/* The same dot by the one-CTA path of the small whole-solve BiCGStab kernel (n <= 8192): k = 1
+ * (out[0] = u0.v0) or 2 (out[1] = u1.v1 too, both in one launch). Test / diagnostics entry. */
+MCR_API int mcr_xdot_cta(int device, int64_t n, const double* u0, const double* v0, const double* u1,
+                         const double* v1, int k, double* out);
+
 /* Use `stream` (a cudaStream_t on the handle's device, or NULL for the handle's own stream)
  * for every later call on this handle. */
 MCR_API int mcr_set_stream(mcr_matrix* m, void* stream);

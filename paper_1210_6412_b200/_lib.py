@@ -35,7 +35,7 @@ EXPORTS = (
     "mcr_chain_info", "mcr_chain_export", "mcr_chain_matrix", "mcr_chain_solve",
     "mcr_shard_enable_p2p", "mcr_read_matrix", "mcr_read_vector", "mcr_read_dtmc",
     "mcr_text_info", "mcr_text_export", "mcr_text_destroy", "mcr_text_reason",
-    "mcr_set_dot_blocks", "mcr_xdot", "mcr_xdot_stats", "mcr_xdot_bench",
+    "mcr_set_dot_blocks", "mcr_xdot", "mcr_xdot_stats", "mcr_xdot_bench", "mcr_xdot_cta",
 )
 MCR_UNSUPPORTED_INPUT = 7
 COMM_ID_BYTES = 128
@@ -108,6 +108,7 @@ def load():
     L.mcr_xdot.argtypes = [ctypes.c_int, i64, vp, vp, ctypes.c_int, vp, vp]
     L.mcr_xdot_stats.argtypes = [vp, vp, ctypes.c_int]
     L.mcr_xdot_bench.argtypes = [ctypes.c_int, i64, vp, vp, ctypes.c_int, ctypes.c_int, vp, vp, vp]
+    L.mcr_xdot_cta.argtypes = [ctypes.c_int, i64, vp, vp, vp, vp, ctypes.c_int, vp]
     L.mcr_matvec.argtypes = [vp, vp, vp]
     L.mcr_matvec_device.argtypes = [vp, vp, vp]
     L.mcr_residual_inf.argtypes = [vp, vp, vp, ctypes.POINTER(dbl)]

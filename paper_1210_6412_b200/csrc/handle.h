@@ -223,6 +223,8 @@ struct mcr_matrix {
     int spmv_grid = 1;
     int small_grid = 0;                     // > 0: whole solve in one cooperative launch
     bool small_cluster = false;             // ... launched as one thread-block cluster
+    bool small_xd = false;                  // ... and its reference-order-dot variant fits too
+    double* xsprod = nullptr;               // that variant's product slots (4n)
     unsigned long long* maxslot = nullptr;  // 3 slots for the persistent solvers
     std::mutex mu;
 

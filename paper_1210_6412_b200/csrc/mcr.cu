@@ -579,6 +579,53 @@ MCR_API int mcr_xdot_bench(int device, int64_t n, const double* u, const double*
     return MCR_OK;
 }
 
+// The one-CTA reference-order dot (k_xdot_cta, small.cuh) stand-alone; test entry point.
+MCR_API int mcr_xdot_cta(int device, int64_t n, const double* u0, const double* v0, const double* u1,
+                         const double* v1, int k, double* out) {
+    if (n < 0 || n > XS_MAX_N || (k != 1 && k != 2) || !out || (n > 0 && (!u0 || !v0)) ||
+        (k == 2 && n > 0 && (!u1 || !v1)))
+        return fail(MCR_INVALID_ARGUMENT, "mcr_xdot_cta: bad arguments");
+    DeviceGuard g(device);
+    cudaStream_t s;
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    std::vector<void*> p;
+    auto done = [&] {
+        for (void* q : p) cudaFreeAsync(q, s);
+        cudaStreamSynchronize(s);
+        cudaStreamDestroy(s);
+    };
+    const size_t bytes = sizeof(double) * (size_t)std::max<int64_t>(n, 1);
+    double* d[5] = {};
+    for (int i = 0; i < 5; ++i) {
+        if (cudaMallocAsync((void**)&d[i], i == 4 ? 2 * sizeof(double) : bytes, s) != cudaSuccess) {
+            done();
+            return fail(MCR_CUDA_ERROR, "mcr_xdot_cta: allocation failed");
+        }
+        p.push_back(d[i]);
+    }
+    const double* src[4] = {u0, v0, k == 2 ? u1 : u0, k == 2 ? v1 : v0};
+    for (int i = 0; i < 4 && n > 0; ++i)
+        cudaMemcpyAsync(d[i], src[i], sizeof(double) * (size_t)n, cudaMemcpyHostToDevice, s);
+    const size_t smem = small_xd_smem(n);
+    cudaError_t e;
+    if (k == 1) {
+        cudaFuncSetAttribute(k_xdot_cta<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_xdot_cta<1><<<1, SM_NT, smem, s>>>(d[0], d[1], d[2], d[3], (int)n, d[4]);
+    } else {
+        cudaFuncSetAttribute(k_xdot_cta<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_xdot_cta<2><<<1, SM_NT, smem, s>>>(d[0], d[1], d[2], d[3], (int)n, d[4]);
+    }
+    e = cudaGetLastError();
+    double h[2] = {0.0, 0.0};
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h, d[4], 2 * sizeof(double), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    done();
+    if (e != cudaSuccess) return fail(MCR_CUDA_ERROR, std::string("mcr_xdot_cta: ") + cudaGetErrorString(e));
+    out[0] = h[0];
+    if (k == 2) out[1] = h[1];
+    return MCR_OK;
+}
+
 MCR_API int mcr_set_stream(mcr_matrix* h, void* stream) {
     if (!h) return fail(MCR_INVALID_ARGUMENT, "NULL handle");
     std::lock_guard<std::mutex> lk(h->mu);

@@ -293,11 +293,26 @@ __global__ void __launch_bounds__(SM_NT) k_jacobi_small(Csr R, Vecs V, SolveStat
 // still read the previous pair while this iteration's is written. Partials live in four
 // separate slots (parts + k*pstride: q.v, t.t, t.s, q.r) because no barrier separates a
 // slot's all-reduce from the next slot's writes. maxslot[2] zero on entry.
-template <bool CL>
-__global__ void __launch_bounds__(SM_NT, 1) k_bicg_small(Csr A, Vecs V, SolveState* st,
+//
+// XD (the default, reference-order dots): the four inner products are the reference's
+// left-to-right sums (solvers.py:136-141) instead of tile partials + a fixed tree. Each row's
+// product goes to a global slot (xprod + k*n; in shared memory directly when the grid is one
+// CTA) before the barrier the partials used; after it every CTA stages the slot in shared
+// memory and computes the same sum with xd::cta_seqdots (all CTAs get identical bits, so no
+// broadcast barrier). Dynamic shared memory: 2n doubles + xd::CtaDots<SM_NT, 2>.
+constexpr int XS_MAX_N = 8192;  // largest system the XD variant takes (2n doubles staged)
+using SmallDots = xd::CtaDots<SM_NT, 2>;
+inline size_t small_xd_smem(long long n) { return (size_t)2 * (size_t)n * sizeof(double) + sizeof(SmallDots); }
+
+template <bool CL, bool XD>
+__global__ void __launch_bounds__(SM_NT, XD ? 2 : 1) k_bicg_small(Csr A, Vecs V, SolveState* st,
                                                       unsigned long long* maxslot, double* parts,
-                                                      int pstride) {
+                                                      int pstride, double* xprod) {
     __shared__ SmallSmem sm;
+    extern __shared__ __align__(16) unsigned char xs_dyn[];
+    double* xbuf = (double*)xs_dyn;  // XD: [2][n]
+    const int n = A.n;
+    SmallDots& xdd = *(SmallDots*)(xs_dyn + (size_t)2 * n * sizeof(double));
     SmallSync<CL> bar;
     const double tol = st->tol;
     const long long max_it = st->max_it;
@@ -329,6 +344,22 @@ __global__ void __launch_bounds__(SM_NT, 1) k_bicg_small(Csr A, Vecs V, SolveSta
         if constexpr (CL) return cluster_read_max(&sm.mx[k], nt);
         else return read_max(&maxslot[k]);
     };
+    // XD: row product of slot k (j = its place in the next cta_seqdots call); after the barrier,
+    // the K consecutive slots from k0 are staged and summed in the reference's order
+    auto put = [&](int k, int j, int r, double p) {
+        if (gridDim.x == 1) xbuf[(size_t)j * n + r] = p;
+        else xprod[(size_t)k * n + r] = p;
+    };
+    auto seqdots = [&](int k0, auto kk, double* res) {
+        constexpr int K = decltype(kk)::value;
+        if (gridDim.x > 1) {
+            for (int i = threadIdx.x; i < K * n; i += SM_NT) xbuf[i] = __ldcg(xprod + (size_t)k0 * n + i);
+            __syncthreads();
+        }
+        xd::cta_seqdots<SM_NT, K>(xbuf, n, *(xd::CtaDots<SM_NT, K>*)&xdd, res);
+    };
+    using One = std::integral_constant<int, 1>;
+    using Two = std::integral_constant<int, 2>;
     double* Rg = V.r;
     load_tile(A, blockIdx.x, sm);
     const int tid = threadIdx.x;
@@ -349,9 +380,12 @@ __global__ void __launch_bounds__(SM_NT, 1) k_bicg_small(Csr A, Vecs V, SolveSta
         V.v[row] = 0.0;
         mb = absbits(ri);
         p1 = dmul(ri, ri);
+        if constexpr (XD) put(S_QR, 0, row, p1);
     }
-    p1 = group_sum<SM_NT / 32, 0>(p1, sm.red);
-    publish(S_QR, Pqr, p1);
+    if constexpr (!XD) {
+        p1 = group_sum<SM_NT / 32, 0>(p1, sm.red);
+        publish(S_QR, Pqr, p1);
+    }
     mb = group_max<SM_NT / 32, 0>(mb, sm.redu);
     publish_max(0, mb);
     bar.sync();
@@ -360,7 +394,9 @@ __global__ void __launch_bounds__(SM_NT, 1) k_bicg_small(Csr A, Vecs V, SolveSta
     double y = 1.0, a = 1.0, w = 1.0, beta = 0.0;
     {
         const double mr = read_maxk(0);
-        const double qr = allreduce(S_QR, Pqr);
+        double qr;
+        if constexpr (XD) seqdots(S_QR, One{}, &qr);
+        else qr = allreduce(S_QR, Pqr);
         if (mr <= tol) {
             stop = CONVERGED;
         } else {
@@ -388,14 +424,19 @@ __global__ void __launch_bounds__(SM_NT, 1) k_bicg_small(Csr A, Vecs V, SolveSta
             Pnew[row] = pi;
             Vnew[row] = vi;
             p1 = dmul(qi, vi);
+            if constexpr (XD) put(S_QV, 0, row, p1);
         }
-        p1 = group_sum<SM_NT / 32, 0>(p1, sm.red);
-        publish(S_QV, Pqv, p1);
+        if constexpr (!XD) {
+            p1 = group_sum<SM_NT / 32, 0>(p1, sm.red);
+            publish(S_QV, Pqv, p1);
+        }
         if constexpr (!CL) {
             if (blockIdx.x == 0 && tid == 0) maxslot[1] = 0ull;
         }
         bar.sync();
-        const double qv = allreduce(S_QV, Pqv);
+        double qv;
+        if constexpr (XD) seqdots(S_QV, One{}, &qv);
+        else qv = allreduce(S_QV, Pqv);
         if (tiny(qv)) { stop = BREAKDOWN; which = 2; bd_it = cur; break; }
         a = ddiv(y, qv);
         // t = M s with s = r - a v formed at each gathered column; s, max|s| for own rows
@@ -411,17 +452,31 @@ __global__ void __launch_bounds__(SM_NT, 1) k_bicg_small(Csr A, Vecs V, SolveSta
             mb = absbits(si);
             p1 = dmul(ti, ti);
             p2 = dmul(ti, si);
+            if constexpr (XD) {
+                put(S_TT, 0, row, p1);
+                put(S_TS, 1, row, p2);
+            }
         }
         mb = group_max<SM_NT / 32, 0>(mb, sm.redu);
         publish_max(1, mb);
-        p1 = group_sum<SM_NT / 32, 0>(p1, sm.red);
-        p2 = group_sum<SM_NT / 32, 0>(p2, sm.red);
-        publish(S_TT, Ptt, p1);
-        publish(S_TS, Pts, p2);
+        if constexpr (!XD) {
+            p1 = group_sum<SM_NT / 32, 0>(p1, sm.red);
+            p2 = group_sum<SM_NT / 32, 0>(p2, sm.red);
+            publish(S_TT, Ptt, p1);
+            publish(S_TS, Pts, p2);
+        }
         bar.sync();
         const bool small = read_maxk(1) <= tol;
-        const double tt = allreduce(S_TT, Ptt);
-        const double ts = allreduce(S_TS, Pts);
+        double tt, ts;
+        if constexpr (XD) {
+            double r2[2];
+            seqdots(S_TT, Two{}, r2);  // slots TT, TS are consecutive
+            tt = r2[0];
+            ts = r2[1];
+        } else {
+            tt = allreduce(S_TT, Ptt);
+            ts = allreduce(S_TS, Pts);
+        }
         if (tiny(tt)) {
             if (!small) { stop = BREAKDOWN; which = 3; bd_it = cur; break; }
             w = 0.0;
@@ -435,14 +490,19 @@ __global__ void __launch_bounds__(SM_NT, 1) k_bicg_small(Csr A, Vecs V, SolveSta
             ri = dsub(si, dmul(w, ti));
             Rg[row] = ri;
             p1 = dmul(qi, ri);
+            if constexpr (XD) put(S_QR, 0, row, p1);
         }
-        p1 = group_sum<SM_NT / 32, 0>(p1, sm.red);
-        publish(S_QR, Pqr, p1);
+        if constexpr (!XD) {
+            p1 = group_sum<SM_NT / 32, 0>(p1, sm.red);
+            publish(S_QR, Pqr, p1);
+        }
         bar.sync();
         it = cur;
         if (small) { stop = CONVERGED; break; }
         if (it >= max_it) { stop = NOTCONV; break; }
-        const double qr = allreduce(S_QR, Pqr);
+        double qr;
+        if constexpr (XD) seqdots(S_QR, One{}, &qr);
+        else qr = allreduce(S_QR, Pqr);
         const double denom = dmul(y, w);
         y = qr;
         if (tiny(denom)) { stop = BREAKDOWN; which = 1; bd_it = it + 1; break; }
@@ -457,5 +517,25 @@ __global__ void __launch_bounds__(SM_NT, 1) k_bicg_small(Csr A, Vecs V, SolveSta
     }
     bar.exit_sync();
 }
+
+// The one-CTA reference-order dot of the small whole-solve kernels (xd::cta_seqdots, the path
+// k_bicg_small<*, true> takes), stand-alone: k = 1 or 2 dots of length n <= XS_MAX_N in one
+// launch (the second pair may alias the first). Test entry point (mcr_xdot_cta).
+template <int K>
+__global__ void __launch_bounds__(SM_NT) k_xdot_cta(const double* u0, const double* v0, const double* u1,
+                                                    const double* v1, int n, double* out) {
+    extern __shared__ __align__(16) unsigned char dyn[];
+    double* buf = (double*)dyn;
+    auto& D = *(xd::CtaDots<SM_NT, K>*)(dyn + (size_t)2 * n * sizeof(double));
+    for (int i = threadIdx.x; i < n; i += SM_NT) {
+        buf[i] = dmul(u0[i], v0[i]);
+        if (K == 2) buf[n + i] = dmul(u1[i], v1[i]);
+    }
+    __syncthreads();
+    double res[K];
+    xd::cta_seqdots<SM_NT, K>(buf, n, D, res);
+    if (threadIdx.x < K) out[threadIdx.x] = res[threadIdx.x];
+}
+
 
 }  // namespace mcr

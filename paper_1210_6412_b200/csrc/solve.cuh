@@ -23,12 +23,13 @@ int read_state(mcr_matrix* h) {
 // ---------------------------------------------------------------- kernel launchers
 // Whole-solve small kernels: one cluster (CL) or one cooperative grid.
 template <typename... KArgs, typename... Args>
-int launch_small(mcr_matrix* h, void (*cluster_kern)(KArgs...), void (*grid_kern)(KArgs...),
+int launch_small(mcr_matrix* h, size_t smem, void (*cluster_kern)(KArgs...), void (*grid_kern)(KArgs...),
                  Args... args) {
     if (h->small_cluster) {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(h->small_grid);
         cfg.blockDim = dim3(SM_NT);
+        cfg.dynamicSmemBytes = smem;
         cfg.stream = h->stream;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -40,7 +41,7 @@ int launch_small(mcr_matrix* h, void (*cluster_kern)(KArgs...), void (*grid_kern
         CK(cudaLaunchKernelEx(&cfg, cluster_kern, static_cast<KArgs>(args)...));
     } else {
         void* a[] = {(void*)&args...};
-        CK(cudaLaunchCooperativeKernel((void*)grid_kern, h->small_grid, SM_NT, a, 0, h->stream));
+        CK(cudaLaunchCooperativeKernel((void*)grid_kern, h->small_grid, SM_NT, a, smem, h->stream));
     }
     return MCR_OK;
 }
@@ -325,7 +326,7 @@ int jacobi_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double tol
     int batch = plan.batch;
     if (h->small_grid > 0) {
         CK(cudaMemsetAsync(h->maxslot, 0, 3 * sizeof(unsigned long long), h->stream));
-        TRY(launch_small(h, k_jacobi_small<true>, k_jacobi_small<false>, csr_off(h), V, h->st,
+        TRY(launch_small(h, 0, k_jacobi_small<true>, k_jacobi_small<false>, csr_off(h), V, h->st,
                          h->maxslot));
         ++launched;
         TRY(read_state(h));
@@ -417,11 +418,18 @@ int bicgstab_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double t
     // max|s| does not decay geometrically (measured: predicted batches overshot by tens of
     // iterations), so BiCGStab keeps the doubling schedule
     int batch = 4;
-    if (h->small_grid > 0 && !h->seqdots) {
+    // reference-order dots on a small system: the XD variant (one CTA per tile sums each
+    // product vector in order itself); the parallel-dot-products blocks take the general path
+    const bool small_xd = h->small_xd && h->seqdots == 1 && h->dot_blocks <= 1;
+    if (h->small_grid > 0 && (!h->seqdots || small_xd)) {
         CK(cudaMemsetAsync(h->maxslot, 0, 3 * sizeof(unsigned long long), h->stream));
         // four partial slots of nunits >= ntiles doubles each (grid variant)
-        TRY(launch_small(h, k_bicg_small<true>, k_bicg_small<false>, csr_full(h), V, h->st,
-                         h->maxslot, h->P, h->nunits));
+        if (small_xd)
+            TRY(launch_small(h, small_xd_smem(h->n), k_bicg_small<true, true>, k_bicg_small<false, true>,
+                             csr_full(h), V, h->st, h->maxslot, h->P, h->nunits, h->xsprod));
+        else
+            TRY(launch_small(h, 0, k_bicg_small<true, false>, k_bicg_small<false, false>, csr_full(h), V,
+                             h->st, h->maxslot, h->P, h->nunits, (double*)nullptr));
         ++launched;
         TRY(read_state(h));
         iters = max_it;  // the loop below has nothing left to do

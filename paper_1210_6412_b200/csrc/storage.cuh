@@ -194,7 +194,9 @@ bool small_cluster_ok(int ctas) {
     if (ok16 < 0) {
         ok16 = cudaFuncSetAttribute(k_jacobi_small<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
                        cudaSuccess &&
-                   cudaFuncSetAttribute(k_bicg_small<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+                   cudaFuncSetAttribute(k_bicg_small<true, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+                       cudaSuccess &&
+                   cudaFuncSetAttribute(k_bicg_small<true, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
                        cudaSuccess;
         cudaGetLastError();
     }
@@ -213,13 +215,55 @@ bool small_cluster_ok(int ctas) {
         int clusters = 0;
         const cudaError_t e = which == 0
                                   ? cudaOccupancyMaxActiveClusters(&clusters, k_jacobi_small<true>, &cfg)
-                                  : cudaOccupancyMaxActiveClusters(&clusters, k_bicg_small<true>, &cfg);
+                                  : cudaOccupancyMaxActiveClusters(&clusters, k_bicg_small<true, false>, &cfg);
         if (e != cudaSuccess || clusters < 1) {
             cudaGetLastError();
             return false;
         }
     }
     return true;
+}
+
+// Can the reference-order-dot variant of k_bicg_small run this handle's small grid (its
+// dynamic shared memory grows with n)? Sets h->small_xd and allocates its product slots.
+int small_xd_check(mcr_matrix* h, int sms) {
+    h->small_xd = false;
+    if (h->n > XS_MAX_N || std::getenv("MCR_NO_SMALL_XD")) return MCR_OK;
+    const size_t smem = small_xd_smem(h->n);
+    if (cudaFuncSetAttribute(k_bicg_small<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess ||
+        cudaFuncSetAttribute(k_bicg_small<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess) {
+        cudaGetLastError();
+        return MCR_OK;
+    }
+    bool ok = false;
+    if (h->small_cluster) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(h->small_grid);
+        cfg.blockDim = dim3(SM_NT);
+        cfg.dynamicSmemBytes = smem;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = h->small_grid;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int clusters = 0;
+        ok = cudaOccupancyMaxActiveClusters(&clusters, k_bicg_small<true, true>, &cfg) == cudaSuccess &&
+             clusters >= 1;
+    } else {
+        int per_sm = 0;
+        ok = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bicg_small<false, true>, SM_NT, smem) ==
+                 cudaSuccess &&
+             per_sm * sms >= h->small_grid;
+    }
+    cudaGetLastError();
+    if (!ok) return MCR_OK;
+    if (h->small_grid > 1) TRY(dalloc(h, &h->xsprod, (size_t)4 * h->n));
+    h->small_xd = true;
+    return MCR_OK;
 }
 
 int init_handle(mcr_matrix* h) {
@@ -243,6 +287,97 @@ int alloc_csr(mcr_matrix* h, int64_t n, int64_t nnz) {
     return MCR_OK;
 }
 
+// Host -> device copies of pageable arrays (a reference CsrMatrix holds plain numpy arrays).
+// cudaMemcpyAsync from pageable memory stages through the driver's own pinned buffer with one
+// host thread; here H2D_THREADS threads each copy their share of the bytes through their own
+// ring of pinned chunks (host memcpy into chunk k while the DMA engine drains chunk k-1), so
+// the host-side copy runs in parallel and overlaps the transfer. Pinned sources and small
+// copies go straight to cudaMemcpyAsync. MCR_H2D_RING=0 turns the ring off.
+struct H2DPart { void* dst; const void* src; size_t bytes; };
+constexpr int H2D_THREADS = 8, H2D_SLOTS = 3;
+constexpr size_t H2D_CHUNK = 4u << 20, H2D_MIN = 8u << 20;
+
+struct H2DRing {
+    std::mutex mu;
+    char* buf[H2D_THREADS][H2D_SLOTS] = {};
+    cudaEvent_t ev[H2D_THREADS][H2D_SLOTS] = {};
+    bool ready = false, failed = false;
+};
+inline H2DRing& h2d_ring() { static H2DRing r; return r; }
+
+inline bool host_pinned(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) { cudaGetLastError(); return false; }
+    return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeManaged;
+}
+
+inline int h2d_copy(const std::vector<H2DPart>& parts, cudaStream_t stream) {
+    static const bool on = [] { const char* e = getenv("MCR_H2D_RING"); return !e || atoi(e) != 0; }();
+    std::vector<H2DPart> ring;
+    size_t total = 0;
+    for (const H2DPart& p : parts) {
+        if (!p.bytes) continue;
+        if (!on || p.bytes < H2D_MIN || host_pinned(p.src)) {
+            CK(cudaMemcpyAsync(p.dst, p.src, p.bytes, cudaMemcpyHostToDevice, stream));
+        } else {
+            ring.push_back(p);
+            total += p.bytes;
+        }
+    }
+    if (ring.empty()) return MCR_OK;
+    H2DRing& R = h2d_ring();
+    std::lock_guard<std::mutex> lock(R.mu);
+    if (!R.ready && !R.failed) {
+        for (int t = 0; t < H2D_THREADS && !R.failed; ++t)
+            for (int s = 0; s < H2D_SLOTS; ++s) {
+                if (cudaHostAlloc((void**)&R.buf[t][s], H2D_CHUNK, cudaHostAllocPortable) != cudaSuccess ||
+                    cudaEventCreateWithFlags(&R.ev[t][s], cudaEventDisableTiming) != cudaSuccess) {
+                    cudaGetLastError();
+                    R.failed = true;
+                    break;
+                }
+            }
+        R.ready = !R.failed;
+    }
+    if (!R.ready) {  // no pinned memory to be had: the driver's own staging
+        for (const H2DPart& p : ring)
+            CK(cudaMemcpyAsync(p.dst, p.src, p.bytes, cudaMemcpyHostToDevice, stream));
+        return MCR_OK;
+    }
+    // thread t copies bytes [t*share, (t+1)*share) of the concatenated parts
+    const size_t share = (total + H2D_THREADS - 1) / H2D_THREADS;
+    std::atomic<int> err{cudaSuccess};
+    int device = 0;
+    CK(cudaGetDevice(&device));
+    auto work = [&](int t) {
+        cudaSetDevice(device);
+        size_t lo = (size_t)t * share, hi = std::min(total, lo + share), base = 0;
+        int slot = 0;
+        for (const H2DPart& p : ring) {
+            const size_t a = std::max(lo, base), b = std::min(hi, base + p.bytes);
+            for (size_t o = a; o < b; o += H2D_CHUNK) {
+                const size_t len = std::min(H2D_CHUNK, b - o);
+                cudaError_t e = cudaEventSynchronize(R.ev[t][slot]);  // the slot's last DMA drained
+                if (e == cudaSuccess) {
+                    memcpy(R.buf[t][slot], (const char*)p.src + (o - base), len);
+                    e = cudaMemcpyAsync((char*)p.dst + (o - base), R.buf[t][slot], len,
+                                        cudaMemcpyHostToDevice, stream);
+                }
+                if (e == cudaSuccess) e = cudaEventRecord(R.ev[t][slot], stream);
+                if (e != cudaSuccess) { err = e; return; }
+                slot = (slot + 1) % H2D_SLOTS;
+            }
+            base += p.bytes;
+        }
+    };
+    std::vector<std::thread> th;
+    for (int t = 1; t < H2D_THREADS; ++t) th.emplace_back(work, t);
+    work(0);
+    for (auto& x : th) x.join();
+    CK((cudaError_t)err.load());
+    return MCR_OK;
+}
+
 int create_impl(mcr_matrix* h, int64_t n, const int64_t* rs, const int64_t* col,
                 const double* val, int storage) {
     NvtxRange range("mcr.create");
@@ -252,10 +387,6 @@ int create_impl(mcr_matrix* h, int64_t n, const int64_t* rs, const int64_t* col,
     tr.mark("create: handle");
     const int64_t nnz = rs[n];
     TRY(alloc_csr(h, n, nnz));
-    CK(cudaMemcpyAsync(h->rp, rs, sizeof(long long) * (size_t)(n + 1), cudaMemcpyHostToDevice,
-                       h->stream));
-    CK(cudaMemcpyAsync(h->val, val, sizeof(double) * (size_t)nnz, cudaMemcpyHostToDevice,
-                       h->stream));
     // int64 columns -> int32 on the device, range-checked, then the row-order check. (A host
     // conversion sending half the bytes was measured slower: the host threads compete with
     // the value copy for host memory bandwidth.)
@@ -265,8 +396,17 @@ int create_impl(mcr_matrix* h, int64_t n, const int64_t* rs, const int64_t* col,
                        h->stream));
     CK(cudaMallocAsync((void**)&bad, 2 * sizeof(int), h->stream));
     CK(cudaMemsetAsync(bad, 0, 2 * sizeof(int), h->stream));
-    CK(cudaMemcpyAsync(tmp, col, sizeof(long long) * (size_t)nnz, cudaMemcpyHostToDevice,
-                       h->stream));
+    // the row tiles are cut on a host thread while the copies run
+    bool monotone = true;
+    long long max_row = 0;
+    std::vector<int> tiles;
+    std::thread cut([&] { tiles = make_tiles(n, rs, &max_row, &monotone); });
+    const int copied = h2d_copy({{h->rp, rs, sizeof(long long) * (size_t)(n + 1)},
+                                 {h->val, val, sizeof(double) * (size_t)nnz},
+                                 {tmp, col, sizeof(long long) * (size_t)nnz}}, h->stream);
+    cut.join();
+    h->max_row = max_row;
+    TRY(copied);
     if (nnz > 0) {
         k_col64to32<<<(int)std::min<int64_t>((nnz + 255) / 256, 1 << 16), 256, 0, h->stream>>>(
             tmp, h->col, nnz, (int)h->n_global, bad);
@@ -274,12 +414,7 @@ int create_impl(mcr_matrix* h, int64_t n, const int64_t* rs, const int64_t* col,
             h->rp, h->col, (int)n, (long long)nnz, bad + 1);
     }
     CK(cudaGetLastError());
-    // the row tiles are cut on the host while the copies are in flight -- before the D2H of the
-    // check flags below, which targets pageable memory and so waits for the stream
-    tr.mark("create: copies issued");
-    bool monotone = true;
-    std::vector<int> tiles = make_tiles(n, rs, &h->max_row, &monotone);
-    tr.mark("create: tiles cut (host)");
+    tr.mark("create: copies issued, tiles cut (host)");
     CK(cudaMemcpyAsync(h->bad_host, bad, 2 * sizeof(int), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaFreeAsync(tmp, h->stream));
     CK(cudaFreeAsync(bad, h->stream));
@@ -432,7 +567,7 @@ int finish_create(mcr_matrix* h, int64_t n, const int64_t* rs, int storage,
                              8.0 * (double)h->n_full() >= auto_bytes));
         int pj = 0, pb = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pj, k_jacobi_small<false>, SM_NT, 0));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pb, k_bicg_small<false>, SM_NT, 0));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pb, k_bicg_small<false, false>, SM_NT, 0));
         const int coresident = sms * std::min(pj, pb);
         // one tile per CTA keeps the per-sweep critical path to a single tile
         if (!h->use_sell && !h->sharded() && !stage && storage != MCR_STORAGE_TILES_STREAM &&
@@ -441,6 +576,7 @@ int finish_create(mcr_matrix* h, int64_t n, const int64_t* rs, int storage,
         // up to 16 tiles: the whole grid as one thread-block cluster (cluster barriers, DSMEM)
         if (h->small_grid > 0 && h->small_grid <= SMALL_CLUSTER_MAX && !std::getenv("MCR_NO_CLUSTER"))
             h->small_cluster = small_cluster_ok(h->small_grid);
+        if (h->small_grid > 0) TRY(small_xd_check(h, sms));
         TRY(dalloc(h, &h->maxslot, 3));
         TRY(dalloc(h, &h->tile_row, tiles.size()));
         CK(cudaMemcpyAsync(h->tile_row, tiles.data(), sizeof(int) * tiles.size(),

@@ -224,18 +224,20 @@ __device__ __forceinline__ bool run_apply(const Run& R, double& v, double& lo, d
 
 // The value v (a partial sum of the carried piece) must stay in its binade, one ulp clear of
 // its ends, under the start shift; zero / subnormal / non-finite: no shift at all.
+// Branch-free; plain compares instead of fmin / fmax (no NaN reaches them: a non-finite v
+// takes the zero range, and lo / hi only ever hold finite values or +-inf).
 __device__ __forceinline__ void value_slack(double v, double& lo, double& hi, int& km) {
     const unsigned long long b = bt(v);
     const int ex = dexp(b);
-    if (ex == 0 || ex == 0x7ff) {
-        lo = fmax(lo, 0.0);
-        hi = fmin(hi, 0.0);
-        return;
-    }
-    const double top = fb(b | MANT), bot = fb((b & ~MANT) | 1ull);  // +-(2^(e+1) - u), +-(2^e + u)
-    lo = fmax(lo, dsub(fmin(top, bot), v));  // exact (same binade)
-    hi = fmin(hi, dsub(fmax(top, bot), v));
-    km = max(km, ex - 1074);
+    const bool special = ex == 0 || ex == 0x7ff;
+    const double t1 = dsub(fb(b | MANT), v);           // +-(2^(e+1) - u) - v, exact (same binade)
+    const double t2 = dsub(fb((b & ~MANT) | 1ull), v); // +-(2^e + u) - v
+    double a = t1 < t2 ? t1 : t2, c = t1 < t2 ? t2 : t1;
+    a = special ? 0.0 : a;
+    c = special ? 0.0 : c;
+    lo = lo > a ? lo : a;
+    hi = hi < c ? hi : c;
+    km = special ? km : max(km, ex - 1074);
 }
 
 __device__ __forceinline__ void sim_step(double& v, double p, double& lo, double& hi, int& km) {
@@ -383,28 +385,30 @@ __device__ __forceinline__ void sim_elems_slow(const double* p, int cnt, double&
     v = x;
 }
 // Branch-free common case: the partial sums fall into at most two binades (the first one's and
-// one other); the extremes are kept per binade. Anything else: the per-stretch path above.
+// one other); the extremes are kept per binade, bucket membership as a bit mask (selects on a
+// predicate compiled to a branch per element). Anything else: the per-stretch path above.
 __device__ __forceinline__ void sim_elems(const double* p, int cnt, double& v, double& lo, double& hi, int& km) {
     if (cnt <= 0) return;
     double x = dadd(v, p[0]);
-    const unsigned long long t0 = bt(x) >> 52;
+    const unsigned t0 = (unsigned)(bt(x) >> 52);
     unsigned long long amin = bt(x), amax = amin, bmin = ~0ull, bmax = 0ull;
 #pragma unroll 4
     for (int k = 1; k < cnt; ++k) {
         x = dadd(x, p[k]);
         const unsigned long long b = bt(x);
-        const bool inA = (b >> 52) == t0;
-        amin = inA ? min(amin, b) : amin;
-        amax = inA ? max(amax, b) : amax;
-        bmin = inA ? bmin : min(bmin, b);
-        bmax = inA ? bmax : max(bmax, b);
+        const unsigned long long mA = 0ull - (unsigned long long)((unsigned)(b >> 52) == t0);
+        amin = min(amin, b | ~mA);
+        amax = max(amax, b & mA);
+        bmin = min(bmin, b | mA);
+        bmax = max(bmax, b & ~mA);
     }
-    if (bmax != 0ull && (bmin >> 52) != (bmax >> 52)) {  // a third binade: redo per stretch
+    const bool has_b = bmin != ~0ull;  // (+0.0 is a member too: test the minimum, not the maximum)
+    if (has_b && (bmin >> 52) != (bmax >> 52)) {  // a third binade: redo per stretch
         sim_elems_slow(p, cnt, v, lo, hi, km);
         return;
     }
     flush_range(amin, amax, lo, hi, km);
-    if (bmax != 0ull) flush_range(bmin, bmax, lo, hi, km);
+    if (has_b) flush_range(bmin, bmax, lo, hi, km);
     v = x;
 }
 
@@ -573,19 +577,11 @@ __device__ double thread_scan(const double* sp, int len, int E, double* s_red, d
     return dadd(wexc, exc);
 }
 
-// All threads: this thread's run (two reference chains in the middle of the binade of `pred`,
-// the predicted start of its elements), then the warp pieces (one merged run when the
-// warp's 32 runs share a binade, else a table around the warp's predicted start). Ends with
-// __syncthreads.
-__device__ void runs_and_warp_pieces(const Scratch& S, const Seq& q, long long c0, int len, int E,
-                                     double pred, unsigned fl, const Smem& M, bool force_table = false) {
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int t0 = tid * E;
-    const int tl = max(0, min(E, len - t0));
-    const double* sp = M.sp;
-#ifdef MCR_XDOT_TIMING
-    const unsigned long long w_t0 = gtime();
-#endif
+// This thread's run over its tl products sp[0..tl): two reference chains from the predicted
+// start (its index made even) and its odd neighbour; HARD unless every partial sum stayed in
+// the prediction's binade, 4096 ulps clear of its ends. `allow` = false (a non-finite
+// product): HARD.
+__device__ __forceinline__ Run thread_run(const double* sp, int tl, double pred, bool allow) {
     Run R = run_empty();
     if (tl > 0) {
         R.e = E_HARD;
@@ -593,7 +589,7 @@ __device__ void runs_and_warp_pieces(const Scratch& S, const Seq& q, long long c
         const int e = dexp(pb);
         const int ng = (int)(pb >> 63);
 #ifndef XD_SKIP_CHAIN
-        if (e >= RUN_MIN_E && e <= 0x7f0 && !(fl & 2u)) {
+        if (e >= RUN_MIN_E && e <= 0x7f0 && allow) {
 #else
         if (false) {
 #endif
@@ -607,7 +603,7 @@ __device__ void runs_and_warp_pieces(const Scratch& S, const Seq& q, long long c
             unsigned long long a0 = bt(ref0), z0 = a0, a1 = bt(ref1), z1 = a1;
 #pragma unroll 4
             for (int k = 0; k < tl; ++k) {
-                const double p = sp[t0 + k];
+                const double p = sp[k];
                 s0 = dadd(s0, p);
                 s1 = dadd(s1, p);
                 a0 = min(a0, bt(s0)); z0 = max(z0, bt(s0));
@@ -634,6 +630,51 @@ __device__ void runs_and_warp_pieces(const Scratch& S, const Seq& q, long long c
             }
         }
     }
+    return R;
+}
+
+// Warp-collective: segments are maximal stretches of thread runs of one binade (a HARD thread
+// is a segment of its own; trailing EMPTY threads join the segment before them). A segmented
+// scan merges each segment into its last lane; returns this lane's merged run and the
+// segment-head mask.
+__device__ __forceinline__ Run warp_merge_runs(const Run& R, int lane, unsigned& heads) {
+    const int pe = __shfl_up_sync(FULL, R.e, 1), pn = __shfl_up_sync(FULL, R.neg, 1);
+    const bool head = lane == 0 || R.e == E_HARD || pe == E_HARD ||
+                      (R.e != E_EMPTY && pe != E_EMPTY && (R.e != pe || R.neg != pn));
+    heads = __ballot_sync(FULL, head);
+    const int seg0 = 31 - __clz(heads & (FULL >> (31 - lane)));  // this lane's segment head
+    Run A = R;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        Run o;
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+            o.d[p] = __shfl_up_sync(FULL, A.d[p], off);
+            o.lo[p] = __shfl_up_sync(FULL, A.lo[p], off);
+            o.hi[p] = __shfl_up_sync(FULL, A.hi[p], off);
+        }
+        o.e = __shfl_up_sync(FULL, A.e, off);
+        o.neg = __shfl_up_sync(FULL, A.neg, off);
+        if (lane - off >= seg0) A = run_merge(o, A);
+    }
+    return A;
+}
+
+// All threads: this thread's run (two reference chains in the middle of the binade of `pred`,
+// the predicted start of its elements), then the warp pieces (one merged run when the
+// warp's 32 runs share a binade, else a table around the warp's predicted start). Ends with
+// __syncthreads.
+__device__ void runs_and_warp_pieces(const Scratch& S, const Seq& q, long long c0, int len, int E,
+                                     double pred, unsigned fl, const Smem& M, bool force_table = false,
+                                     bool first = false) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int t0 = tid * E;
+    const int tl = max(0, min(E, len - t0));
+    const double* sp = M.sp;
+#ifdef MCR_XDOT_TIMING
+    const unsigned long long w_t0 = gtime();
+#endif
+    const Run R = thread_run(sp + t0, tl, pred, !(fl & 2u));
     M.runs[tid] = R;
 #ifdef MCR_XDOT_DEBUG
     if (R.e != E_HARD && R.e != E_EMPTY) {
@@ -657,28 +698,8 @@ __device__ void runs_and_warp_pieces(const Scratch& S, const Seq& q, long long c
     const unsigned long long w_t1 = gtime();
     if (lane == 0 && S.stats) atomicMax(S.stats + ST_W_CHAIN, w_t1 - w_t0);
 #endif
-    // Segments: maximal stretches of thread runs of one binade (a HARD thread is a segment of
-    // its own; trailing EMPTY threads join the segment before them). A segmented scan merges
-    // each segment into its last lane.
-    const int pe = __shfl_up_sync(FULL, R.e, 1), pn = __shfl_up_sync(FULL, R.neg, 1);
-    const bool head = lane == 0 || R.e == E_HARD || pe == E_HARD ||
-                      (R.e != E_EMPTY && pe != E_EMPTY && (R.e != pe || R.neg != pn));
-    const unsigned heads = __ballot_sync(FULL, head);
-    const int seg0 = 31 - __clz(heads & (FULL >> (31 - lane)));  // this lane's segment head
-    Run A = R;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        Run o;
-#pragma unroll
-        for (int p = 0; p < 2; ++p) {
-            o.d[p] = __shfl_up_sync(FULL, A.d[p], off);
-            o.lo[p] = __shfl_up_sync(FULL, A.lo[p], off);
-            o.hi[p] = __shfl_up_sync(FULL, A.hi[p], off);
-        }
-        o.e = __shfl_up_sync(FULL, A.e, off);
-        o.neg = __shfl_up_sync(FULL, A.neg, off);
-        if (lane - off >= seg0) A = run_merge(o, A);
-    }
+    unsigned heads;
+    const Run A = warp_merge_runs(R, lane, heads);
     const unsigned ends = (heads >> 1) | 0x80000000u;  // last lane of each segment
     const double wpred = __shfl_sync(FULL, pred, 0);
     Desc* WD = M.wd + warp;
@@ -693,11 +714,12 @@ __device__ void runs_and_warp_pieces(const Scratch& S, const Seq& q, long long c
         const int wn = window_neg(wpred);
         double v = cand(mb0, wn, lane), lo = -INFINITY, hi = INFINITY;
         int km = KM_NONE;
-        // a warp of mostly element-by-element threads (the sum passing near zero): its table
-        // could not be shifted anyway (the start's low bits decide the roundings on the way
-        // up), so only the values are carried -- the root walks such a stretch from its exact
-        // start when it needs it
-        const bool bare = false;  // (carrying values only measured slower: more root walks)
+        // The first warp of a sequence starts at exactly 0.0 (its prediction, and candidate 0 of
+        // its window): only that lane's value is ever used, so the lanes carry values alone
+        // (plain adds, no slack bookkeeping; every other candidate is served at delta = 0 only).
+        // (Carrying values only in other element-by-element warps measured slower: their
+        // starts are not known, so the root walked them.)
+        const bool bare = first && warp == 0;
 #ifdef XD_TWICE
         for (int rep = 0; rep < 2; ++rep) {
         const unsigned long long tr0 = gtime();
@@ -874,7 +896,7 @@ __device__ int build_cta(const Args& A, const Seq& q, int si, const Smem& M, dou
     XT_ADD(S, ST_T_LOOKBACK, t_lb);
     XT_MARK(t_runs);
     if (A.upto == 2) return ci;
-    runs_and_warp_pieces(S, q, c0, len, E, dadd(pred_cta, exc), fl, M, A.upto == 13);
+    runs_and_warp_pieces(S, q, c0, len, E, dadd(pred_cta, exc), fl, M, A.upto == 13, ci == 0);
     XT_ADD(S, ST_T_RUNS, t_runs);
     XT_MARK(t_cta);
     if (A.upto == 3 || A.upto == 13) return ci;
@@ -1266,6 +1288,228 @@ __device__ bool xdot_body(const Args& A, double* d) {
         for (int s = 0; s < A.nseq; ++s) A.out[2 + s] = __ldcg(A.S.result + s);
     }
     return true;
+}
+
+// ---------------------------------------------------------------- one CTA, whole sequence
+// For the whole-solve small kernels (small.cuh): K product arrays of length n in shared memory
+// (buf + k*n), one CTA of NTH threads; every thread receives the K reference-order sums.
+// Thread runs and warp segments as above (predictions from a plain block scan), then lane 0 of
+// warp k walks dot k from 0.0 through the warp segments: a segment's merged run where it
+// applies to the true value, its products one by one where it does not (a HARD thread is a
+// segment of its own). No tables are needed: the walk always holds the exact value, so the
+// result is the reference's bits for every input. The walk is one dependent chain, so it
+// advances four segments at a time speculatively (each step only needs the value's parity)
+// and checks the four steps' conditions afterwards; a group with a failed check is redone
+// segment by segment.
+// A segment as the walker reads it: 16-byte pairs (one vector load each, then a select on the
+// value's parity -- a per-half load would put the shared-memory latency on the walk's chain).
+struct __align__(16) SegRun {
+    double2 d, lo, hi;
+    int e, neg;
+    int i0, i1;  // its products [i0, i1)
+};
+
+template <int NTH, int K>
+struct CtaDots {
+    SegRun seg[K][NTH];          // per warp, its segments (compacted)
+    int cnt[K][NTH / 32];        // segments per warp
+    double red[K][NTH / 32];     // warp totals of the plain sums
+    unsigned wfl[K][NTH / 32];   // warp flags: bit 0 a product that is not -0.0, bit 1 non-finite
+    double out[K];
+};
+
+// One segment from the exact value v: the run's value at v; ok = the run applies (v in the
+// run's binade, every partial sum one ulp clear of its ends).
+__device__ __forceinline__ double seg_step(const SegRun& R, double v, bool& ok) {
+    const double2 d = R.d, l = R.lo, h = R.hi;
+    const unsigned long long b = bt(v);
+    const bool odd = (b & 1ull) != 0;
+    const double vn = dadd(v, odd ? d.y : d.x);
+    const int ng = (int)(b >> 63);
+    const double vlo = dadd(v, odd ? l.y : l.x), vhi = dadd(v, odd ? h.y : h.x);
+    const double bot = fb(((unsigned long long)ng << 63) | ((unsigned long long)R.e << 52) | 1ull);
+    const double top = fb(((unsigned long long)ng << 63) | ((unsigned long long)R.e << 52) | MANT);
+    const bool in = ng ? (vhi <= bot && vlo >= top) : (vlo >= bot && vhi <= top);
+    ok = dexp(b) == R.e && ng == R.neg && in;
+    return vn;
+}
+
+// plain left-to-right sum of p[i0, i1) onto v (8 loads ahead of the add chain)
+__device__ __forceinline__ double walk_elems(const double* p, int i0, int i1, double v) {
+    int i = i0;
+    for (; i + 8 <= i1; i += 8) {
+        double x[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] = p[i + j];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v = dadd(v, x[j]);
+    }
+    const int r = i1 - i;  // 0..7 left: all loads first (a load per add would chain the latency)
+    double x[7];
+#pragma unroll
+    for (int j = 0; j < 7; ++j) x[j] = j < r ? p[i + j] : 0.0;
+#pragma unroll
+    for (int j = 0; j < 7; ++j)
+        if (j < r) v = dadd(v, x[j]);
+    return v;
+}
+
+constexpr int XS_SERIAL_MAX = 384;  // up to this many products one thread just adds them
+
+template <int NTH, int K>
+__device__ void cta_seqdots(const double* buf, int n, CtaDots<NTH, K>& D, double* res) {
+    constexpr int NWS = NTH / 32;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#ifdef MCR_XS_TIMING
+    const long long xt0 = clock64();
+    long long xt1 = xt0, xt2 = xt0;
+    int nseg = 0, nwalk = 0;
+#endif
+    if (n <= XS_SERIAL_MAX) {  // the walk alone costs less than building runs
+        if (lane == 0 && warp < K) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                if (k != warp) continue;
+                const double* p = buf + (size_t)k * n;
+                double v = walk_elems(p, 0, n, 0.0);
+                // cumsum starts from p_0 itself: -0.0 survives only when every product is -0.0
+                if (v == 0.0 && n > 0) {
+                    bool allneg0 = true;
+                    for (int i = 0; i < n; ++i) allneg0 &= bt(p[i]) == SGN;
+                    if (allneg0) v = -0.0;
+                }
+                D.out[k] = v;
+            }
+        }
+    } else {
+        const int E = (n + NTH - 1) / NTH;
+        const int t0 = tid * E, tl = max(0, min(E, n - t0));
+        double pred[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const double* p = buf + (size_t)k * n + t0;
+            double ts = 0.0;
+            unsigned fl = 0u;
+            for (int i = 0; i < tl; ++i) {
+                const double x = p[i];
+                const unsigned long long b = bt(x);
+                ts = dadd(ts, x);
+                fl |= (b != SGN ? 1u : 0u) | (dexp(b) == 0x7ff ? 2u : 0u);
+            }
+            double inc = ts;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const double o = __shfl_up_sync(FULL, inc, off);
+                if (lane >= off) inc = dadd(inc, o);
+            }
+            const double exc = __shfl_up_sync(FULL, inc, 1);
+            pred[k] = lane == 0 ? 0.0 : exc;
+            fl = __reduce_or_sync(FULL, fl);
+            if (lane == 31) {
+                D.red[k][warp] = inc;
+                D.wfl[k][warp] = fl;
+            }
+        }
+        __syncthreads();
+#ifdef MCR_XS_TIMING
+        xt1 = clock64();
+#endif
+        unsigned flags[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            double wexc = 0.0;
+            unsigned fl = 0u;
+#pragma unroll
+            for (int w = 0; w < NWS; ++w) {
+                const double r = D.red[k][w];
+                if (w < warp) wexc = dadd(wexc, r);
+                fl |= D.wfl[k][w];
+            }
+            flags[k] = fl;
+            const Run R = thread_run(buf + (size_t)k * n + t0, tl, dadd(wexc, pred[k]), !(fl & 2u));
+            unsigned hd;
+            const Run A = warp_merge_runs(R, lane, hd);
+            const unsigned ends = (hd >> 1) | 0x80000000u;
+            // segments made of EMPTY threads only (past the end of the products) are dropped;
+            // they come after every other segment, so the compaction keeps the order
+            const unsigned live = __ballot_sync(FULL, ((ends >> lane) & 1u) && A.e != E_EMPTY);
+            if ((live >> lane) & 1u) {  // compact: segment j = lanes [first, lane]
+                const unsigned before = ends & ((1u << lane) - 1u);
+                const int first = before ? 32 - __clz(before) : 0;
+                SegRun& S = D.seg[k][warp * 32 + __popc(live & ((1u << lane) - 1u))];
+                S.d = make_double2(A.d[0], A.d[1]);
+                S.lo = make_double2(A.lo[0], A.lo[1]);
+                S.hi = make_double2(A.hi[0], A.hi[1]);
+                S.e = A.e;
+                S.neg = A.neg;
+                S.i0 = (warp * 32 + first) * E;
+                S.i1 = min(n, (warp * 32 + lane + 1) * E);
+            }
+            if (lane == 0) D.cnt[k][warp] = __popc(live);
+        }
+        __syncthreads();
+#ifdef MCR_XS_TIMING
+        xt2 = clock64();
+#endif
+        if (lane == 0 && warp < K) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                if (k != warp) continue;
+                const double* p = buf + (size_t)k * n;
+                double v = 0.0;
+                for (int w = 0; w < NWS; ++w) {
+                    const int cnt = D.cnt[k][w];
+                    const SegRun* sg = &D.seg[k][w * 32];
+#ifdef MCR_XS_TIMING
+                    nseg += cnt;
+#endif
+                    // a warp of many short segments: its products one by one are cheaper
+                    if (cnt * 4 > min(n, (w + 1) * 32 * E) - w * 32 * E) {
+                        v = walk_elems(p, w * 32 * E, min(n, (w + 1) * 32 * E), v);
+#ifdef MCR_XS_TIMING
+                        nwalk += min(n, (w + 1) * 32 * E) - w * 32 * E;
+#endif
+                        continue;
+                    }
+                    // the next segment is loaded while this one is applied (its shared-memory
+                    // latency stays off the value's dependency chain); a HARD segment (e = 0)
+                    // never matches the exponent of a value that a run could apply to
+                    SegRun cur = sg[0];
+                    for (int j = 0; j < cnt; ++j) {
+                        const SegRun nxt = sg[min(j + 1, cnt - 1)];
+                        bool ok;
+                        const double vn = seg_step(cur, v, ok);
+                        if (ok && cur.e != E_HARD) {
+                            v = vn;
+                        } else {
+                            v = walk_elems(p, cur.i0, cur.i1, v);
+#ifdef MCR_XS_TIMING
+                            nwalk += cur.i1 - cur.i0;
+#endif
+                        }
+                        cur = nxt;
+                    }
+                }
+                // cumsum starts from p_0 itself: -0.0 survives only when every product is -0.0
+                if (v == 0.0 && !(flags[k] & 1u)) v = -0.0;
+                D.out[k] = v;
+            }
+        }
+    }
+#ifdef MCR_XS_TIMING
+    const long long xt3 = clock64();
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        static __device__ int xs_calls = 0;
+        if (xs_calls < 12) {
+            ++xs_calls;
+            printf("xs n=%d K=%d: runs %lld merge %lld walk %lld cycles, segments %d, walked %d\n", n, K,
+                   xt1 - xt0, xt2 - xt1, xt3 - xt2, nseg, nwalk);
+        }
+    }
+#endif
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; ++k) res[k] = D.out[k];
 }
 
 }  // namespace xd

@@ -60,3 +60,31 @@ def dot_stats(u, v, nblocks: int = 1, device: int = 0):
     before the library was first used."""
     out, st = _run(u, v, nblocks, device, True)
     return float(out[0]), st
+
+
+CTA_MAX_N = 8192
+
+
+def dot_ascending_cta(u, v, u2=None, v2=None, device: int = 0):
+    """The same sum(s) by the one-CTA path of the small whole-solve BiCGStab kernel
+    (n <= 8192; a second pair u2, v2 is summed in the same launch): a float, or a pair."""
+    pairs = [(u, v)] + ([(u2, v2)] if u2 is not None else [])
+    arrs = []
+    for a, b in pairs:
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        if a.shape != b.shape or a.ndim != 1 or a.shape != np.shape(pairs[0][0]):
+            raise ValueError("dot_ascending_cta: shapes")
+        arrs += [a, b]
+    if arrs[0].size > CTA_MAX_N:
+        raise ValueError(f"dot_ascending_cta: n <= {CTA_MAX_N}")
+    k = len(pairs)
+    if k == 1:
+        arrs += [arrs[0], arrs[1]]
+    out = np.zeros(2)
+    L = _lib.load()
+    rc = L.mcr_xdot_cta(int(device), int(arrs[0].size), *(a.ctypes.data for a in arrs), k, out.ctypes.data)
+    if rc != _lib.MCR_OK:
+        raise _lib.NativeLibraryError(f"libmcr error {rc}: {_lib.last_error()}")
+    return float(out[0]) if k == 1 else (float(out[0]), float(out[1]))
+

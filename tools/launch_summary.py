@@ -4,7 +4,7 @@ rows = list(csv.reader(open(sys.argv[1])))
 hi = next(i for i, r in enumerate(rows) if 'Kernel Name' in r)
 h = rows[hi]; data = rows[hi + 1:]
 ki = h.index('Kernel Name'); mi = h.index('Metric Name'); vi = h.index('Metric Value'); ui = h.index('Metric Unit')
-scale = {'nsecond': 1e-3, 'usecond': 1.0, 'msecond': 1e3, 'second': 1e6}
+scale = {'nsecond': 1e-3, 'usecond': 1.0, 'msecond': 1e3, 'second': 1e6, 'ns': 1e-3, 'us': 1.0, 'ms': 1e3, 's': 1e6}
 agg = collections.defaultdict(list)
 for r in data:
     if r[mi] == 'gpu__time_duration.sum':

@@ -18,6 +18,17 @@ KEYS = {
     "block": "launch__block_size",
     "smem_bank_conflicts": "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
     "sm_clock_mhz": "smsp__cycles_elapsed.avg.per_second",
+    # the L2 <-> SM path the x gathers use
+    "l1tex2xbar_req_cycles_active_pct": "l1tex__m_l1tex2xbar_req_cycles_active.avg.pct_of_peak_sustained_elapsed",
+    "l1tex2xbar_req_cycles_active_max_pct": "l1tex__m_l1tex2xbar_req_cycles_active.max.pct_of_peak_sustained_elapsed",
+    "xbar2l1tex_read_bytes": "l1tex__m_xbar2l1tex_read_bytes.sum",
+    "xbar2l1tex_read_bytes_pct": "l1tex__m_xbar2l1tex_read_bytes.sum.pct_of_peak_sustained_elapsed",
+    "xbar2l1tex_read_sectors_pct": "l1tex__m_xbar2l1tex_read_sectors.avg.pct_of_peak_sustained_elapsed",
+    "xbar2l1tex_tma_bytes": "l1tex__m_xbar2l1tex_read_bytes_mem_global_op_tma_ld.sum",
+    "xbar2l1tex_ldg_sectors": "l1tex__m_xbar2l1tex_read_sectors_mem_lg_op_ld.sum",
+    "lts_throughput_pct": "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+    "l1tex_throughput_pct": "l1tex__throughput.avg.pct_of_peak_sustained_elapsed",
+    "sm_warps_active_pct": "sm__warps_active.avg.pct_of_peak_sustained_active",
 }
 UNITS = {"ns": 1e-3, "us": 1.0, "ms": 1e3, "byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1,
          "msecond": 1e3, "second": 1e6, "hz": 1e-6, "Khz": 1e-3, "Mhz": 1, "Ghz": 1e3}
@@ -54,7 +65,7 @@ def rep_summary(rep):
                     v = float(r[i].replace(",", ""))
                 except ValueError:
                     continue
-                d[k] = v * UNITS.get(u[i], 1.0) if k in ("duration_us", "dram_read_bytes", "dram_write_bytes", "sm_clock_mhz") else v
+                d[k] = v * UNITS.get(u[i], 1.0) if k in ("duration_us", "dram_read_bytes", "dram_write_bytes", "sm_clock_mhz", "xbar2l1tex_read_bytes", "xbar2l1tex_tma_bytes") else v
         per[short(r[h.index("Kernel Name")])].append(d)
     kern = {}
     for k, lst in per.items():
