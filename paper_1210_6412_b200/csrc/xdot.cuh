@@ -365,23 +365,37 @@ __device__ __forceinline__ void flush_range(unsigned long long bmin, unsigned lo
     value_slack(fb(bmin), lo, hi, km);
     value_slack(fb(bmax), lo, hi, km);
 }
+// Any number of binades: every partial sum's own constraint, branch-free (lanes whose sums
+// change binade at different elements do not diverge) and light on the integer pipe, which
+// is what limits this loop when a whole CTA runs it: with lo <= 0 <= hi always, each bound is
+// tracked as the smallest distance to the binade end a shift of that sign reaches, by the
+// high word of the distance only (the low word dropped: a slightly smaller distance, so the
+// bounds only get narrower -- always safe).
 __device__ __forceinline__ void sim_elems_slow(const double* p, int cnt, double& v, double& lo, double& hi, int& km) {
-    if (cnt <= 0) return;
-    double x = dadd(v, p[0]);
-    unsigned long long bmin = bt(x), bmax = bmin, top = bmin >> 52;
-    for (int k = 1; k < cnt; ++k) {
+    double x = v;
+    unsigned lom = (unsigned)__double2hiint(lo) & 0x7fffffffu, him = (unsigned)__double2hiint(hi) & 0x7fffffffu;
+    int kmx = km;
+#pragma unroll 4
+    for (int k = 0; k < cnt; ++k) {
         x = dadd(x, p[k]);
-        const unsigned long long b = bt(x);
-        if ((b >> 52) != top) {
-            flush_range(bmin, bmax, lo, hi, km);
-            bmin = bmax = b;
-            top = b >> 52;
-        } else {
-            bmin = min(bmin, b);
-            bmax = max(bmax, b);
-        }
+        const unsigned h = (unsigned)__double2hiint(x);
+        const unsigned e = (h >> 20) & 0x7ffu;
+        const bool special = e - 1u >= 0x7feu;  // zero / subnormal / inf / nan: no shift at all
+        const bool neg = (int)h < 0;
+        const unsigned hb = h & 0xfff00000u;
+        // a negative shift moves a positive sum toward its binade's bottom (significand 1), a
+        // negative sum toward its top (all ones); a positive shift the other way
+        const double to_lo = __hiloint2double((int)(hb | (neg ? 0xfffffu : 0u)), (int)(neg ? 0xffffffffu : 1u));
+        const double to_hi = __hiloint2double((int)(hb | (neg ? 0u : 0xfffffu)), (int)(neg ? 1u : 0xffffffffu));
+        const unsigned da = (unsigned)__double2hiint(dsub(to_lo, x)) & 0x7fffffffu;  // exact differences
+        const unsigned dc = (unsigned)__double2hiint(dsub(to_hi, x)) & 0x7fffffffu;
+        lom = min(lom, special ? 0u : da);
+        him = min(him, special ? 0u : dc);
+        kmx = special ? kmx : max(kmx, (int)e - 1074);
     }
-    flush_range(bmin, bmax, lo, hi, km);
+    lo = -__hiloint2double((int)lom, 0);
+    hi = __hiloint2double((int)him, 0);
+    km = kmx;
     v = x;
 }
 // Branch-free common case: the partial sums fall into at most two binades (the first one's and
@@ -414,10 +428,25 @@ __device__ __forceinline__ void sim_elems(const double* p, int cnt, double& v, d
 
 // Per lane, no collectives: carry v through the thread runs [t0, t1) of the CTA range in shared
 // memory, adding a thread's products one by one where its run does not apply.
+//
+// `q` (> 0): 32 ulps of the binade of this lane's candidate start. A table entry is looked up
+// either at its candidate exactly or at a start 32k ulps away (k != 0), so once the entry's
+// shift range [lo, hi] lies inside (-q, q) -- the sum passed close to zero, where the grid is
+// fine -- it can serve its candidate alone: the range is set to [0, 0] and the rest of the walk
+// carries the value only (plain adds instead of the slack bookkeeping).
+__device__ __forceinline__ double quantum32(double c) {
+    const int e = max(dexp(bt(c)), 1);
+    return e >= 48 ? fb((unsigned long long)(e - 47) << 52) : ldexp(32.0, e - 1075);
+}
 __device__ void lane_walk_threads(const Run* s_runs, const double* sp, int len, int E, int t0, int t1,
                                   double& v, double& lo, double& hi, int& km,
-                                  unsigned long long* sims = nullptr, bool bare = false) {
+                                  unsigned long long* sims = nullptr, bool bare = false, double q = 0.0) {
     for (int t = t0; t < t1; ++t) {
+        if (!bare && lo > -q && hi < q) {
+            bare = true;
+            lo = 0.0;
+            hi = 0.0;
+        }
         const Run R = s_runs[t];
         if (run_apply(R, v, lo, hi, km)) continue;
         const int b0 = t * E, bl = max(0, min(E, len - b0));
@@ -425,9 +454,12 @@ __device__ void lane_walk_threads(const Run* s_runs, const double* sp, int len, 
         if (sims) atomicAdd(sims, 1ull);
 #endif
         if (bare) {  // the value only: this lane then serves its exact start alone
+#pragma unroll 4
             for (int k = 0; k < bl; ++k) v = dadd(v, sp[b0 + k]);
             lo = fmax(lo, 0.0);
             hi = fmin(hi, 0.0);
+        } else if (R.e == E_HARD) {  // its sums change binade: the per-sum path straight away
+            sim_elems_slow(sp + b0, bl, v, lo, hi, km);
         } else {
             sim_elems(sp + b0, bl, v, lo, hi, km);
         }
@@ -714,6 +746,7 @@ __device__ void runs_and_warp_pieces(const Scratch& S, const Seq& q, long long c
         const int wn = window_neg(wpred);
         double v = cand(mb0, wn, lane), lo = -INFINITY, hi = INFINITY;
         int km = KM_NONE;
+        const double q32 = quantum32(v);
         // The first warp of a sequence starts at exactly 0.0 (its prediction, and candidate 0 of
         // its window): only that lane's value is ever used, so the lanes carry values alone
         // (plain adds, no slack bookkeeping; every other candidate is served at delta = 0 only).
@@ -753,7 +786,7 @@ __device__ void runs_and_warp_pieces(const Scratch& S, const Seq& q, long long c
 #endif
             if (!okr)
                 lane_walk_threads(M.runs, sp, len, E, warp * 32 + sl, warp * 32 + el + 1, v, lo, hi, km,
-                                  S.stats ? S.stats + ST_SIMS_WARP : nullptr, bare);
+                                  S.stats ? S.stats + ST_SIMS_WARP : nullptr, bare, q32);
 #ifdef MCR_XDOT_TIMING
             __syncwarp();
             cyc_walk += clock64() - c_b;
@@ -820,13 +853,15 @@ __device__ void compose_pair(const Smem& M, int len, int E, const Desc* L, const
         neg = window_neg(hl.pred);
         v = cand(mb0, neg, lane);
         if (!run_apply(hdr_run(hl), v, lo, hi, km)) {
-            if (walk) lane_walk_threads(M.runs, M.sp, len, E, t0, t1, v, lo, hi, km);
+            if (walk) lane_walk_threads(M.runs, M.sp, len, E, t0, t1, v, lo, hi, km, nullptr, false,
+                                        quantum32(cand(mb0, neg, lane)));
             else hole = 1;
         }
     }
     const PieceR P = load_piece(R);
     if (!piece_apply_r(P, v, lo, hi, km) && !hole) {  // collective; then per lane
-        if (walk) lane_walk_threads(M.runs, M.sp, len, E, t1, t2, v, lo, hi, km);
+        if (walk) lane_walk_threads(M.runs, M.sp, len, E, t1, t2, v, lo, hi, km, nullptr, false,
+                                    quantum32(cand(mb0, neg, lane)));
         else hole = 1;
     }
     LaneR Lx;
