@@ -725,6 +725,25 @@ __device__ void runs_and_warp_pieces(const Scratch& S, const Seq& q, long long c
     }
 #endif
     if (R.e == E_HARD && S.stats) stat(S, ST_HARD);
+#ifdef MCR_XDOT_TIMING
+    {  // distribution of HARD threads: max per warp (DBG_TAB), max per CTA (DBG_SPARE), CTAs with
+       // more than 64 (DBG_TR_BAD), warps with more than 8 (DBG_TAB_BAD)
+        const int wh = __popc(__ballot_sync(FULL, R.e == E_HARD));
+        __shared__ int s_hard;
+        if (threadIdx.x == 0) s_hard = 0;
+        __syncthreads();
+        if (lane == 0 && wh) atomicAdd(&s_hard, wh);
+        if (lane == 0 && S.stats) {
+            atomicMax(S.stats + ST_DBG_TAB, (unsigned long long)wh);
+            if (wh > 8) atomicAdd(S.stats + ST_DBG_TAB_BAD, 1ull);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && S.stats) {
+            atomicMax(S.stats + ST_DBG_SPARE, (unsigned long long)s_hard);
+            if (s_hard > 64) atomicAdd(S.stats + ST_DBG_TR_BAD, 1ull);
+        }
+    }
+#endif
     __syncwarp();
 #ifdef MCR_XDOT_TIMING
     const unsigned long long w_t1 = gtime();

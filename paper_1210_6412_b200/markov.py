@@ -33,8 +33,9 @@ from .sparse import CsrMatrix
 __all__ = ["ChainSystem", "build_system", "partition_states", "reachability_probabilities",
            "METHODS", "MarkovChainError"]
 
-# method name -> (mcr_chain_solve method, reference-order dots)
-METHODS = {"jacobi-gpu": (0, 0), "bicgstab-gpu": (1, 0), "bicgstab-gpu-exact": (1, 1)}
+# method name -> (mcr_chain_solve method, reference-order dots: None = the config's
+# dot_products, "sequential" by default, as the solvers of solvers.py)
+METHODS = {"jacobi-gpu": (0, 0), "bicgstab-gpu": (1, None), "bicgstab-gpu-exact": (1, 1)}
 
 
 def _reference():
@@ -129,6 +130,8 @@ class ChainSystem:
         except KeyError:
             raise ValueError(f"unknown method {method!r}, expected one of {sorted(METHODS)}") from None
         cfg = config or SolverConfig()
+        if dots is None:
+            dots = 0 if getattr(cfg, "dot_products", "sequential") == "tree" else 1
         x0 = None
         seed = getattr(cfg, "guess_seed", None)
         if seed is not None and self.k:  # solvers.py:153-156 on the reduced system
