@@ -379,25 +379,24 @@ __device__ __forceinline__ void sim_elems_slow(const double* p, int cnt, double&
     for (int k = 0; k < cnt; ++k) {
         x = dadd(x, p[k]);
         const unsigned h = (unsigned)__double2hiint(x);
-        const unsigned e = (h >> 20) & 0x7ffu;
-        const bool special = e - 1u >= 0x7feu;  // zero / subnormal / inf / nan: no shift at all
-        const bool neg = (int)h < 0;
-        const unsigned hb = h & 0xfff00000u;
-        // a negative shift moves a positive sum toward its binade's bottom (significand 1), a
-        // negative sum toward its top (all ones); a positive shift the other way
-        const double to_lo = __hiloint2double((int)(hb | (neg ? 0xfffffu : 0u)), (int)(neg ? 0xffffffffu : 1u));
-        const double to_hi = __hiloint2double((int)(hb | (neg ? 0u : 0xfffffu)), (int)(neg ? 1u : 0xffffffffu));
-        const unsigned da = (unsigned)__double2hiint(dsub(to_lo, x)) & 0x7fffffffu;  // exact differences
-        const unsigned dc = (unsigned)__double2hiint(dsub(to_hi, x)) & 0x7fffffffu;
-        lom = min(lom, special ? 0u : da);
-        him = min(him, special ? 0u : dc);
-        kmx = special ? kmx : max(kmx, (int)e - 1074);
+        const unsigned hb = h & 0x7ff00000u;  // |x|'s binade: bottom end (hb, 1), top end (hb | 0xfffff, ~0)
+        const double ax = fabs(x);
+        const unsigned d_bot = (unsigned)__double2hiint(dsub(ax, __hiloint2double((int)hb, 1)));  // exact, >= 0
+        const unsigned d_top = (unsigned)__double2hiint(dsub(__hiloint2double((int)(hb | 0xfffffu), -1), ax));
+        // a negative shift moves a positive sum toward its bottom end, a negative sum toward its top
+        const unsigned sgn = (unsigned)((int)h >> 31);
+        const unsigned to_lo = (d_top & sgn) | (d_bot & ~sgn), to_hi = (d_bot & sgn) | (d_top & ~sgn);
+        // zero / subnormal: no shift at all (inf / nan: the entry becomes a hole anyway)
+        lom = min(lom, hb ? to_lo : 0u);
+        him = min(him, hb ? to_hi : 0u);
+        kmx = max(kmx, (int)(hb >> 20) - 1074);
     }
     lo = -__hiloint2double((int)lom, 0);
     hi = __hiloint2double((int)him, 0);
     km = kmx;
     v = x;
 }
+
 // Branch-free common case: the partial sums fall into at most two binades (the first one's and
 // one other); the extremes are kept per binade, bucket membership as a bit mask (selects on a
 // predicate compiled to a branch per element). Anything else: the per-stretch path above.
