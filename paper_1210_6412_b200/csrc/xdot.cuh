@@ -449,9 +449,6 @@ __device__ void lane_walk_threads(const Run* s_runs, const double* sp, int len, 
         const Run R = s_runs[t];
         if (run_apply(R, v, lo, hi, km)) continue;
         const int b0 = t * E, bl = max(0, min(E, len - b0));
-#ifdef MCR_XDOT_TIMING
-        if (sims) atomicAdd(sims, 1ull);
-#endif
         if (bare) {  // the value only: this lane then serves its exact start alone
 #pragma unroll 4
             for (int k = 0; k < bl; ++k) v = dadd(v, sp[b0 + k]);
