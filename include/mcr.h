@@ -230,6 +230,21 @@ MCR_API int mcr_generate_rhs(const mcr_matrix* m, uint64_t seed, double* d_b);
  * nonzero[nnz]); any pointer may be NULL. */
 MCR_API int mcr_matrix_export(mcr_matrix* m, int64_t* rstart, int64_t* col, double* nonzero);
 
+/* The reference's input generator on the device, drawing numpy's default_rng(seed) stream:
+ * generate_dd_matrix (S/generator.py:100-124, off-diagonal codes by _sample_off_diagonal
+ * :77-97) with `count` = target_nnz - n off-diagonal entries and values in [lo, hi] -- the same
+ * arrays as the reference, directly into a device handle. pcg = {state >> 64, state & (2^64-1),
+ * inc >> 64, inc & (2^64-1)} of numpy's PCG64(seed) (the Python wrapper computes it). */
+MCR_API int mcr_refgen_matrix(int device, int64_t n, int64_t count, int64_t lo, int64_t hi,
+                              const uint64_t* pcg, int storage, mcr_matrix** out);
+/* default_rng(seed).integers(lo, hi, size=n, endpoint=True) as doubles into host `out`
+ * (generate_rhs, S/generator.py:127-132: lo = 1, hi = 10). */
+MCR_API int mcr_refgen_integers(int device, int64_t n, int64_t lo, int64_t hi, const uint64_t* pcg,
+                                double* out);
+/* default_rng(seed).integers(0, range, size=n) into host `out` (range >= 2): the bounded draw of
+ * either width, rejections included. Test / diagnostics entry. */
+MCR_API int mcr_refgen_u64(int device, int64_t n, uint64_t range, const uint64_t* pcg, uint64_t* out);
+
 /* ---------------------------------------------------------------------------------------
  * Reachability of a Markov chain: the caller side of the solve,
  * build_system + reachability_probabilities (markov.py:152-293), on the device.

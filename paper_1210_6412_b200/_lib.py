@@ -36,6 +36,7 @@ EXPORTS = (
     "mcr_shard_enable_p2p", "mcr_read_matrix", "mcr_read_vector", "mcr_read_dtmc",
     "mcr_text_info", "mcr_text_export", "mcr_text_destroy", "mcr_text_reason",
     "mcr_set_dot_blocks", "mcr_xdot", "mcr_xdot_stats", "mcr_xdot_bench", "mcr_xdot_cta",
+    "mcr_refgen_matrix", "mcr_refgen_integers", "mcr_refgen_u64",
 )
 MCR_UNSUPPORTED_INPUT = 7
 COMM_ID_BYTES = 128
@@ -109,6 +110,9 @@ def load():
     L.mcr_xdot_stats.argtypes = [vp, vp, ctypes.c_int]
     L.mcr_xdot_bench.argtypes = [ctypes.c_int, i64, vp, vp, ctypes.c_int, ctypes.c_int, vp, vp, vp]
     L.mcr_xdot_cta.argtypes = [ctypes.c_int, i64, vp, vp, vp, vp, ctypes.c_int, vp]
+    L.mcr_refgen_matrix.argtypes = [ctypes.c_int, i64, i64, i64, i64, vp, ctypes.c_int, ctypes.POINTER(vp)]
+    L.mcr_refgen_integers.argtypes = [ctypes.c_int, i64, i64, i64, vp, vp]
+    L.mcr_refgen_u64.argtypes = [ctypes.c_int, i64, ctypes.c_uint64, vp, vp]
     L.mcr_matvec.argtypes = [vp, vp, vp]
     L.mcr_matvec_device.argtypes = [vp, vp, vp]
     L.mcr_residual_inf.argtypes = [vp, vp, vp, ctypes.POINTER(dbl)]

@@ -13,6 +13,7 @@
 #include "storage.cuh"
 #include "solve.cuh"
 #include "chain_host.cuh"
+#include "refgen_host.cuh"
 
 using namespace mcr;
 
@@ -295,6 +296,77 @@ MCR_API int mcr_generate_rhs(const mcr_matrix* h, uint64_t seed, double* d_b) {
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(h->stream));
     return MCR_OK;
+}
+
+// The reference's generator on the device (refgen.cuh): pcg = {state >> 64, state, inc >> 64,
+// inc} of numpy's PCG64(seed) (default_rng(seed).bit_generator.state).
+MCR_API int mcr_refgen_matrix(int device, int64_t n, int64_t count, int64_t lo, int64_t hi, const uint64_t* pcg,
+                              int storage, mcr_matrix** out) {
+    if (!pcg || !out || n < 1 || count < 0 || lo < 1 || hi < lo || hi - lo >= (1ll << 31) ||
+        (n > 1 && count > n * (n - 1)) || (n == 1 && count > 0) || n >= (1ll << 31))
+        return fail(MCR_INVALID_ARGUMENT, "mcr_refgen_matrix: bad arguments");
+    DeviceGuard g(device);
+    cudaStream_t st;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    RgStream S;
+    S.s = rg::mk128(pcg[0], pcg[1]);
+    S.inc = rg::mk128(pcg[2], pcg[3]);
+    long long* rp = nullptr;
+    int* col = nullptr;
+    double* val = nullptr;
+    int rc = rg_matrix(st, S, n, count, lo, hi, &rp, &col, &val);
+    if (rc == MCR_OK) rc = create_from_device(n, count + n, rp, col, val, device, storage, out);
+    if (rp) cudaFreeAsync(rp, st);
+    if (col) cudaFreeAsync(col, st);
+    if (val) cudaFreeAsync(val, st);
+    cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+    return rc;
+}
+
+MCR_API int mcr_refgen_integers(int device, int64_t n, int64_t lo, int64_t hi, const uint64_t* pcg, double* out) {
+    if (!pcg || !out || n < 0 || hi < lo || hi - lo > 0xFFFFFFFEll)
+        return fail(MCR_INVALID_ARGUMENT, "mcr_refgen_integers: bad arguments");
+    if (n == 0) return MCR_OK;
+    DeviceGuard g(device);
+    cudaStream_t st;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    RgStream S;
+    S.s = rg::mk128(pcg[0], pcg[1]);
+    S.inc = rg::mk128(pcg[2], pcg[3]);
+    double* d = nullptr;
+    int rc = MCR_OK;
+    if (cudaMallocAsync((void**)&d, sizeof(double) * (size_t)n, st) != cudaSuccess)
+        rc = fail(MCR_CUDA_ERROR, "mcr_refgen_integers: allocation failed");
+    if (rc == MCR_OK) rc = rg_draw(st, S, (uint64_t)(hi - lo + 1), lo, n, nullptr, d);
+    if (rc == MCR_OK && cudaMemcpyAsync(out, d, sizeof(double) * (size_t)n, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+        rc = fail(MCR_CUDA_ERROR, "mcr_refgen_integers: copy failed");
+    if (d) cudaFreeAsync(d, st);
+    cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+    return rc;
+}
+
+MCR_API int mcr_refgen_u64(int device, int64_t n, uint64_t range, const uint64_t* pcg, uint64_t* out) {
+    if (!pcg || !out || n < 0 || range < 2) return fail(MCR_INVALID_ARGUMENT, "mcr_refgen_u64: bad arguments");
+    if (n == 0) return MCR_OK;
+    DeviceGuard g(device);
+    cudaStream_t st;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    RgStream S;
+    S.s = rg::mk128(pcg[0], pcg[1]);
+    S.inc = rg::mk128(pcg[2], pcg[3]);
+    uint64_t* d = nullptr;
+    int rc = MCR_OK;
+    if (cudaMallocAsync((void**)&d, sizeof(uint64_t) * (size_t)n, st) != cudaSuccess)
+        rc = fail(MCR_CUDA_ERROR, "mcr_refgen_u64: allocation failed");
+    if (rc == MCR_OK) rc = rg_draw(st, S, range, 0, n, d, nullptr);
+    if (rc == MCR_OK && cudaMemcpyAsync(out, d, sizeof(uint64_t) * (size_t)n, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+        rc = fail(MCR_CUDA_ERROR, "mcr_refgen_u64: copy failed");
+    if (d) cudaFreeAsync(d, st);
+    cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+    return rc;
 }
 
 MCR_API int mcr_matrix_export(mcr_matrix* h, int64_t* rstart, int64_t* col, double* nonzero) {

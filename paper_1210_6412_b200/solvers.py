@@ -163,6 +163,23 @@ class DeviceMatrix:
             _raise_native(rc)
         return cls(None, _handle=h)
 
+    @classmethod
+    def reference_generated(cls, spec, device: int = 0, storage: int = _lib.STORAGE_AUTO):
+        """``generate_dd_matrix(spec)`` (S/generator.py:100-124) drawn on the device from the
+        reference's own random stream (mcr_refgen_matrix): the same arrays, straight into HBM."""
+        from .generator import pcg_words
+        n = int(spec.n)
+        count = int(spec.target_nnz()) - n
+        lo, hi = spec.value_range
+        words = pcg_words(spec.seed)
+        L = _lib.load()
+        h = ctypes.c_void_p()
+        rc = L.mcr_refgen_matrix(int(device), n, count, int(lo), int(hi), words.ctypes.data, int(storage),
+                                 ctypes.byref(h))
+        if rc != _lib.MCR_OK:
+            _raise_native(rc)
+        return cls(None, _handle=h)
+
     def generated_rhs(self, seed: int, out_device_ptr: int) -> None:
         rc = self._L.mcr_generate_rhs(self._h, int(seed), ctypes.c_void_p(out_device_ptr))
         if rc != _lib.MCR_OK:
