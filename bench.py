@@ -565,11 +565,18 @@ def run_c5(args):
     L = _lib.load()
     n, mean, seed = args.n, 7.0, 2024
     t_gen = time.perf_counter()
+    refgen = world == 1 and args.gen == "reference"
     if world > 1:
         comm = Comm.nccl(local)
         h = ShardMatrix.generated(comm, n, mean, 1, 10, seed, storage=STORAGES[args.storage])
         if args.p2p:
             h.enable_p2p()
+    elif refgen:  # the reference's generator and random stream (GenSpec(n, nnz=8n), trial 0)
+        from paper_1210_6412_b200.generator import GenSpec, generate_rhs_device, trial_seed
+        comm = None
+        seed = trial_seed(0, n, None, 8 * n, 0)
+        h = DeviceMatrix.reference_generated(GenSpec(n=n, nnz=8 * n, seed=seed), device=local,
+                                             storage=STORAGES[args.storage])
     else:
         comm = None
         h = DeviceMatrix.generated(n, mean, 1, 10, seed, device=local, storage=STORAGES[args.storage])
@@ -578,8 +585,13 @@ def run_c5(args):
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
     L.mcr_set_stream(h.handle, ctypes.c_void_p(stream.cuda_stream))
+    if world == 1:
+        L.mcr_set_dot_mode(h.handle, _lib.DOT_MODES[args.dots])
     b = torch.empty(rows, dtype=torch.float64, device=dev)
-    h.generated_rhs(seed, b.data_ptr())
+    if refgen:
+        b.copy_(torch.from_numpy(generate_rhs_device(n, seed, local)))
+    else:
+        h.generated_rhs(seed, b.data_ptr())
     x = torch.empty(rows, dtype=torch.float64, device=dev)
     torch.cuda.synchronize()
     t_gen = time.perf_counter() - t_gen
@@ -676,10 +688,15 @@ def run_c5(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic: row-keyed device generator of the reference's DD family (C5)",
-        "config": {"workload": f"C5: n={n}, ~8 nnz/row (1 + Poisson(7)), row-sharded over {world} GPU(s)",
+        "data": ("synthetic: the reference's generate_dd_matrix / generate_rhs drawn on the device from "
+                 "numpy's default_rng stream (mcr_refgen_matrix; the same arrays the reference would build)"
+                 if refgen else "synthetic: row-keyed device generator of the reference's DD family (C5)"),
+        "config": {"workload": (f"C5: GenSpec(n={n}, nnz={8 * n}, seed=trial_seed(0, n, None, nnz, 0))"
+                                if refgen else
+                                f"C5: n={n}, ~8 nnz/row (1 + Poisson(7)), row-sharded over {world} GPU(s)"),
                    "n": n, "nnz": nnz, "tolerance": 1e-10,
-                   "solve_pair": "jacobi + bicgstab (tree dots) from x0=0",
+                   "solve_pair": ("jacobi + bicgstab from x0=0, BiCGStab dots: "
+                                  + (args.dots if world == 1 else "tree (rank-order)")),
                    "l2": "inputs (x 1.6 GB, matrix ~19 GB) far larger than L2",
                    "parallelism": (f"row shards x{world} ("
                                    + ("fused P2P stores + NCCL slot exchange" if args.p2p and world > 1
@@ -864,6 +881,9 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c5"])
     ap.add_argument("--n", type=int, default=2 * 10 ** 8, help="C5 dimension")
+    ap.add_argument("--gen", default="reference", choices=["reference", "rowkeyed"],
+                    help="C5 inputs on one GPU: the reference's generator and stream (default) or the "
+                         "row-keyed shard generator (always used at N > 1)")
     ap.add_argument("--p2p", action="store_true",
                     help="C5 at N > 1: fused exchange (producers store into peers' copies)")
     ap.add_argument("--no-cpu-baseline", action="store_true")

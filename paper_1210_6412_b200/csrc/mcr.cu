@@ -336,7 +336,7 @@ MCR_API int mcr_refgen_integers(int device, int64_t n, int64_t lo, int64_t hi, c
     S.inc = rg::mk128(pcg[2], pcg[3]);
     double* d = nullptr;
     int rc = MCR_OK;
-    if (cudaMallocAsync((void**)&d, sizeof(double) * (size_t)n, st) != cudaSuccess)
+    if (cudaMallocAsync((void**)&d, sizeof(double) * (size_t)rg_cap(n), st) != cudaSuccess)
         rc = fail(MCR_CUDA_ERROR, "mcr_refgen_integers: allocation failed");
     if (rc == MCR_OK) rc = rg_draw(st, S, (uint64_t)(hi - lo + 1), lo, n, nullptr, d);
     if (rc == MCR_OK && cudaMemcpyAsync(out, d, sizeof(double) * (size_t)n, cudaMemcpyDeviceToHost, st) != cudaSuccess)
@@ -358,7 +358,7 @@ MCR_API int mcr_refgen_u64(int device, int64_t n, uint64_t range, const uint64_t
     S.inc = rg::mk128(pcg[2], pcg[3]);
     uint64_t* d = nullptr;
     int rc = MCR_OK;
-    if (cudaMallocAsync((void**)&d, sizeof(uint64_t) * (size_t)n, st) != cudaSuccess)
+    if (cudaMallocAsync((void**)&d, sizeof(uint64_t) * (size_t)rg_cap(n), st) != cudaSuccess)
         rc = fail(MCR_CUDA_ERROR, "mcr_refgen_u64: allocation failed");
     if (rc == MCR_OK) rc = rg_draw(st, S, range, 0, n, d, nullptr);
     if (rc == MCR_OK && cudaMemcpyAsync(out, d, sizeof(uint64_t) * (size_t)n, cudaMemcpyDeviceToHost, st) != cudaSuccess)

@@ -23,7 +23,9 @@
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_select.cuh>
+#include <cub/device/device_reduce.cuh>
 #include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
 
 namespace mcr {
 namespace rg {
@@ -54,6 +56,10 @@ __host__ __device__ __forceinline__ uint64_t pcg_out(u128 s) {
 }
 
 constexpr int RAW_PER_THREAD = 64;
+
+struct ToLL {
+    __host__ __device__ long long operator()(unsigned char c) const { return (long long)c; }
+};
 
 // 64-bit Lemire draws for raw positions [j0, j0 + cnt): value (valid where accepted) and the
 // accept flag. re = range size (rng + 1), th = (2^64 - re) % re.

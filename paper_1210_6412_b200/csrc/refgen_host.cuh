@@ -40,9 +40,14 @@ inline int rg_grid(long long items) {
     return (int)std::max<long long>(1, std::min<long long>((items + 255) / 256, 1 << 20));
 }
 
+// Output capacity rg_draw needs for `need` draws (the compaction writes every accepted draw of
+// its batch, a little more than needed).
+inline long long rg_cap(long long need) { return need + need / 64 + 4096; }
+
 // `need` accepted bounded draws of range size `re` (values offset by `lo`) continuing the stream
 // at S: 64-bit Lemire on raw outputs when re - 1 > 2^32 - 1, else 32-bit Lemire on halves.
-// Appends the values (as uint64 codes, or as doubles when `dout`) and advances S.
+// Writes the values (as uint64 codes, or as doubles when `dout`; rg_cap(need) capacity) and
+// advances S.
 int rg_draw(cudaStream_t st, RgStream& S, uint64_t re, long long lo, long long need, uint64_t* uout,
             double* dout) {
     if (need <= 0) return MCR_OK;
@@ -52,7 +57,7 @@ int rg_draw(cudaStream_t st, RgStream& S, uint64_t re, long long lo, long long n
     long long got = 0;
     while (got < need) {
         const long long want = need - got;
-        const long long cnt = want + want / 64 + 4096;  // rejections are rare (< re / 2^bits)
+        const long long cnt = rg_cap(want);  // rejections are rare (< re / 2^bits)
         unsigned char *ok = nullptr, *rej = nullptr;
         TRY(mem.get(&ok, (size_t)cnt));
         uint64_t* uv = nullptr;
@@ -75,17 +80,23 @@ int rg_draw(cudaStream_t st, RgStream& S, uint64_t re, long long lo, long long n
         TRY(mem.get(&nsel, 1));
         TRY(mem.get(&nrej, 1));
         TRY(mem.get(&rej, (size_t)cnt));
-        TRY(mem.get(&rpos, (size_t)cnt));
         rg::k_not<<<rg_grid(cnt), 256, 0, st>>>(ok, cnt, rej);
-        thrust::counting_iterator<long long> iota(0);
+        // how many were rejected (sized before the positions are listed)
+        thrust::transform_iterator<rg::ToLL, const unsigned char*> rej_ll(rej, rg::ToLL());
         size_t tmp = 0;
-        CK(cub::DeviceSelect::Flagged(nullptr, tmp, iota, rej, rpos, nrej, cnt, st));
+        CK(cub::DeviceReduce::Sum(nullptr, tmp, rej_ll, nrej, cnt, st));
         void* dtmp = nullptr;
         TRY(mem.get((unsigned char**)&dtmp, tmp));
-        CK(cub::DeviceSelect::Flagged(dtmp, tmp, iota, rej, rpos, nrej, cnt, st));
+        CK(cub::DeviceReduce::Sum(dtmp, tmp, rej_ll, nrej, cnt, st));
         long long h_nrej = 0;
         CK(cudaMemcpyAsync(&h_nrej, nrej, sizeof(long long), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
+        TRY(mem.get(&rpos, (size_t)h_nrej));
+        thrust::counting_iterator<long long> iota(0);
+        tmp = 0;
+        CK(cub::DeviceSelect::Flagged(nullptr, tmp, iota, rej, rpos, nrej, cnt, st));
+        TRY(mem.get((unsigned char**)&dtmp, tmp));
+        CK(cub::DeviceSelect::Flagged(dtmp, tmp, iota, rej, rpos, nrej, cnt, st));
         const long long acc = cnt - h_nrej, take = std::min(acc, want);
         // stream position after the take-th accepted draw: take + rejections before it
         std::vector<long long> rp((size_t)h_nrej);
@@ -101,18 +112,16 @@ int rg_draw(cudaStream_t st, RgStream& S, uint64_t re, long long lo, long long n
         else CK(cub::DeviceSelect::Flagged(nullptr, tmp2, dv, ok, dv, nsel, cnt, st));
         void* dtmp2 = nullptr;
         TRY(mem.get((unsigned char**)&dtmp2, tmp2));
+        // (outputs hold rg_cap(need) >= got + cnt entries: the compaction writes all accepted)
         if (wide) {
-            uint64_t* sel = nullptr;
-            TRY(mem.get(&sel, (size_t)acc));
-            CK(cub::DeviceSelect::Flagged(dtmp2, tmp2, uv, ok, sel, nsel, cnt, st));
-            CK(cudaMemcpyAsync(uout + got, sel, sizeof(uint64_t) * (size_t)take, cudaMemcpyDeviceToDevice, st));
+            CK(cub::DeviceSelect::Flagged(dtmp2, tmp2, uv, ok, uout + got, nsel, cnt, st));
+        } else if (dout) {
+            CK(cub::DeviceSelect::Flagged(dtmp2, tmp2, dv, ok, dout + got, nsel, cnt, st));
         } else {
             double* sel = nullptr;
             TRY(mem.get(&sel, (size_t)acc));
             CK(cub::DeviceSelect::Flagged(dtmp2, tmp2, dv, ok, sel, nsel, cnt, st));
-            if (dout) {
-                CK(cudaMemcpyAsync(dout + got, sel, sizeof(double) * (size_t)take, cudaMemcpyDeviceToDevice, st));
-            } else {  // codes of the 32-bit path: doubles holding integers < 2^32
+            {  // codes of the 32-bit path: doubles holding integers < 2^32
                 rg::k_d2u<<<rg_grid(take), 256, 0, st>>>(sel, take, uout + got);
                 CK(cudaGetLastError());
             }
@@ -146,7 +155,7 @@ int rg_codes(cudaStream_t st, RgStream& S, long long total, long long count, uin
     for (;;) {
         const long long b = std::max<long long>(1024, 2 * (count - have));
         uint64_t* codes = nullptr;
-        TRY(mem.get(&codes, (size_t)(drawn + b)));
+        TRY(mem.get(&codes, (size_t)(drawn + rg_cap(b))));
         long long off = 0;
         for (size_t i = 0; i < batches.size(); ++i) {  // the earlier batches, in draw order
             CK(cudaMemcpyAsync(codes + off, batches[i], sizeof(uint64_t) * (size_t)sizes[i], cudaMemcpyDeviceToDevice, st));
@@ -209,9 +218,9 @@ int rg_matrix(cudaStream_t st, RgStream& S, long long n, long long count, long l
     RgMem mem{st, {}};
     uint64_t* codes = nullptr;
     double *vals = nullptr, *slack = nullptr;
-    TRY(mem.get(&codes, (size_t)count));
-    TRY(mem.get(&vals, (size_t)count));
-    TRY(mem.get(&slack, (size_t)n));
+    TRY(mem.get(&codes, (size_t)rg_cap(count)));
+    TRY(mem.get(&vals, (size_t)rg_cap(count)));
+    TRY(mem.get(&slack, (size_t)rg_cap(n)));
     TRY(rg_codes(st, S, total, count, codes));                                   // :110
     TRY(rg_draw(st, S, (uint64_t)(hi - lo + 1), lo, count, nullptr, vals));      // :115
     TRY(rg_draw(st, S, (uint64_t)hi, 1, n, nullptr, slack));                     // :117
