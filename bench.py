@@ -544,6 +544,17 @@ def c5_cpu_proxy(threads: int, n_proxy: int, sweeps: int, n_full: int, iters: di
                         f"at 2.5 sweeps each): extrapolated, not run")
 
 
+def c5_traffic(storage, n):
+    """DRAM bytes of one C5 SpMV from the committed ncu capture (profiles/r01_c5_staged_ncu.json:
+    both staged passes, n = 2e8), or None for another size or the tiled layout."""
+    from paper_1210_6412_b200 import _lib
+    if storage != _lib.STORAGE_STAGED or n != 2 * 10 ** 8:
+        return None
+    a = load_traffic("k_stage_products<0>", "c5_staged")
+    b = load_traffic("k_spmv_staged<0>", "c5_staged")
+    return a + b if a is not None and b is not None else None
+
+
 def run_c5(args):
     import ctypes
 
@@ -705,7 +716,7 @@ def run_c5(args):
         "iterations": iters,
         "time_to_solution_ms": {"jacobi": rj.device_seconds * 1e3, "bicgstab": rb.device_seconds * 1e3},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None,
+                     "frac": achieved / peak, "traffic": c5_traffic(info["storage"], n),
                      "kernel": ("k_stage_products + k_spmv_staged (band-staged SpMV, both passes)"
                                 if info["storage"] == _lib.STORAGE_STAGED else "k_spmv<EPI_Y>")
                                + " on this rank's rows",
