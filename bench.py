@@ -742,7 +742,8 @@ def run_c5(args):
 def run_sharded(args):
     """N GPUs on ONE system: the C1/C2/C3 system's rows split contiguously over N shards
     (the reference's _row_blocks up to +-1 row), Jacobi bit-identical to one GPU,
-    BiCGStab with rank-order inner products (the reference-order dots run on one GPU).
+    BiCGStab with the reference's dot order (every shard sums the gathered vectors; --dots tree:
+    per-rank trees combined in rank order).
     Under torchrun (WORLD_SIZE = N) one process per GPU with NCCL; otherwise one process
     drives N shards as threads (devices from MCR_GPU_DEVICES, e.g. 0,0 puts two shards on one
     GPU, else 0..N-1) with the in-process transport. Strong scaling: value = solves of the one
@@ -792,7 +793,7 @@ def run_sharded(args):
             sh = ShardMatrix.from_matrix(comms[r], m)
             stream = torch.cuda.Stream(dev)
             sh.set_stream(stream.cuda_stream)
-            L.mcr_set_dot_mode(sh.handle, _lib.DOTS_TREE)
+            sh.set_dots("tree" if args.dots == "tree" else "sequential")
             bl = torch.from_numpy(np.ascontiguousarray(b[sh.row0:sh.row0 + sh.n])).to(dev)
             xl = torch.empty(sh.n, dtype=torch.float64, device=dev)
 
@@ -863,7 +864,10 @@ def run_sharded(args):
         "data": "synthetic: reference generator (bit-identical to mcreach.generate_dd_matrix)",
         "config": {"workload": desc + f", rows sharded over {world} GPU(s)", "n": n, "nnz": nnz,
                    "tolerance": 1e-10,
-                   "solve_pair": "jacobi (bit-identical) + bicgstab (rank-order inner products) from x0=0",
+                   "solve_pair": ("jacobi + bicgstab from x0=0, both bit-identical to one GPU and the "
+                                  "reference (BiCGStab dots: every shard sums the gathered vectors in the "
+                                  "reference's order)" if args.dots != "tree" else
+                                  "jacobi (bit-identical) + bicgstab (tree dots, rank-order) from x0=0"),
                    "l2": "inputs resident in HBM",
                    "parallelism": f"row shards x{world}: allgather of the iterate / p / s + "
                                   f"rank-order scalar exchange; {transport}"},

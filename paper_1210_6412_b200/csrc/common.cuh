@@ -74,6 +74,8 @@ struct SolveState {
                   //    partials in send[] instead of finalising; k_finalize finishes after the
                   //    per-rank exchange
     double send[SEND_SLOTS];  // {dot 1, dot 2, max|.| as bits, unused} of this rank
+    double xd[2];             // row shard, reference-order dots: k_xdot's sums of the whole
+                              // gathered vectors (identical on every rank), read by k_finalize
 };
 
 // Entry range [e0, e1) and row range [r0, r1) of one tile.

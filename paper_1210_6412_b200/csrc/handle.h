@@ -96,7 +96,7 @@ struct DeviceGuard {
 // Work vectors. FULL ones are gather inputs of the SpMV and span the whole system when the
 // matrix is a row shard (world * chunk entries, indexed by global row); the others hold this
 // handle's rows only. On one GPU both kinds are n long.
-enum { V_X = 0, V_X1, V_P, V_S, V_FULL_COUNT, V_B = V_FULL_COUNT, V_R, V_Q, V_V, V_T, V_COUNT };
+enum { V_X = 0, V_X1, V_P, V_S, V_R, V_Q, V_V, V_T, V_FULL_COUNT, V_B = V_FULL_COUNT, V_COUNT };
 
 }  // namespace
 
@@ -301,12 +301,14 @@ Vecs base_vecs(const mcr_matrix* h) {
     V.b = h->vec(V_B);
     V.d = h->d;
     V.x = h->vec(V_X) + h->roff;
-    V.r = h->vec(V_R);
-    V.q = h->vec(V_Q);
+    // r, q, v, t are full length too: on a row shard with reference-order dots they are
+    // gathered and every rank sums the whole vectors (sharded xdot_prepare)
+    V.r = h->vec(V_R) + h->roff;
+    V.q = h->vec(V_Q) + h->roff;
     V.p = h->vec(V_P) + h->roff;
-    V.v = h->vec(V_V);
+    V.v = h->vec(V_V) + h->roff;
     V.s = h->vec(V_S) + h->roff;
-    V.t = h->vec(V_T);
+    V.t = h->vec(V_T) + h->roff;
     V.P1 = h->P;
     V.P2 = h->P + h->nunits;
     V.x_jac0 = h->vec(V_X);

@@ -556,8 +556,8 @@ MCR_API int mcr_set_dot_mode(mcr_matrix* h, int mode) {
     if (mode != MCR_DOTS_TREE && mode != MCR_DOTS_SEQUENTIAL && mode != MCR_DOTS_SERIAL)
         return fail(MCR_INVALID_ARGUMENT, "unknown dot mode");
     std::lock_guard<std::mutex> lk(h->mu);
-    if (mode != MCR_DOTS_TREE && h->sharded())
-        return fail(MCR_INVALID_ARGUMENT, "sequential dots need the whole system on one GPU");
+    if (mode == MCR_DOTS_SERIAL && h->sharded())
+        return fail(MCR_INVALID_ARGUMENT, "serial dots need the whole system on one GPU");
     h->seqdots = mode;
     return MCR_OK;
 }

@@ -119,10 +119,15 @@ int xdot_prepare(mcr_matrix* h, const Vecs& V) {
     TRY(xdot_smem_attr<SQ_V>());
     TRY(xdot_smem_attr<SQ_T>());
     TRY(xdot_smem_attr<SQ_E>());
-    TRY(xdot_plan(X, SQ_S0, h->stream, h->device, h->n, 1, nb, V.r, V.r, nullptr, nullptr));
-    TRY(xdot_plan(X, SQ_V, h->stream, h->device, h->n, 1, nb, V.q, V.v, nullptr, nullptr));
-    TRY(xdot_plan(X, SQ_T, h->stream, h->device, h->n, 2, nb, V.t, V.t, V.t, V.s));
-    TRY(xdot_plan(X, SQ_E, h->stream, h->device, h->n, 1, nb, V.q, V.r, nullptr, nullptr));
+    // a row shard sums the whole gathered vectors (every rank the same bits): its own rows sit
+    // at roff of the full-length buffers
+    const int64_t n = h->sharded() ? h->n_global : h->n;
+    const double *q = V.q - h->roff, *r = V.r - h->roff, *v = V.v - h->roff, *t = V.t - h->roff,
+                 *s = V.s - h->roff;
+    TRY(xdot_plan(X, SQ_S0, h->stream, h->device, n, 1, nb, r, r, nullptr, nullptr));
+    TRY(xdot_plan(X, SQ_V, h->stream, h->device, n, 1, nb, q, v, nullptr, nullptr));
+    TRY(xdot_plan(X, SQ_T, h->stream, h->device, n, 2, nb, t, t, t, s));
+    TRY(xdot_plan(X, SQ_E, h->stream, h->device, n, 1, nb, q, r, nullptr, nullptr));
     return MCR_OK;
 }
 
@@ -436,6 +441,10 @@ int bicgstab_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double t
     } else {
         // r = b - 1.0 * M x0, q = r, p = v = 0
         launch_mv<EPI_S0>(h, false, h->vec(V_X), V, &launched);
+        if (sh && h->seqdots) {  // the whole r and q (= r) for the dots
+            TRY(allgather_full(h, h->vec(V_R)));
+            TRY(allgather_full(h, h->vec(V_Q)));
+        }
         launch_seqdot<SQ_S0>(h, V, &launched);
         TRY(launch_check());
         if (sh) TRY(exchange_point<FIN_S0>(h, nullptr, &launched));
@@ -456,14 +465,17 @@ int bicgstab_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double t
             launch_phase<PH_A>(h, V, &launched);               // p = r + beta (p - w v)
             if (sh) TRY(h->p2p ? p2p_barrier(h) : allgather_full(h, p_full));
             launch_mv<EPI_V>(h, false, p_full, V, &launched);  // v = M p, q.v -> a
+            if (sh && h->seqdots) TRY(allgather_full(h, h->vec(V_V)));
             launch_seqdot<SQ_V>(h, V, &launched);
             if (sh) TRY(exchange_point<FIN_V>(h, nullptr, &launched));
             launch_phase<PH_C>(h, V, &launched);               // s = r - a v, max|s|
             if (sh) TRY(h->p2p ? p2p_barrier(h) : allgather_full(h, s_full));
             launch_mv<EPI_T>(h, false, s_full, V, &launched);  // t = M s, t.t, t.s -> w
+            if (sh && h->seqdots) TRY(allgather_full(h, h->vec(V_T)));
             launch_seqdot<SQ_T>(h, V, &launched);
             if (sh) TRY(exchange_point<FIN_T>(h, nullptr, &launched));
             launch_phase<PH_E>(h, V, &launched);               // x, r updates, q.r -> beta
+            if (sh && h->seqdots) TRY(allgather_full(h, h->vec(V_R)));
             launch_seqdot<SQ_E>(h, V, &launched);
             if (sh) TRY(exchange_point<FIN_E>(h, nullptr, &launched));
         }

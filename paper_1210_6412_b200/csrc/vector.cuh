@@ -211,6 +211,10 @@ __global__ void k_finalize(SolveState* st, const double* __restrict__ recv, int 
     } else if constexpr (W == FIN_RESID) {
         st->resid = bits2d(mb);
     } else {
+        if (st->seqdots) {  // reference-order dots of the whole gathered vectors (k_xdot)
+            d1 = st->xd[0];
+            d2 = st->xd[1];
+        }
         st->maxbits = mb;  // read (and cleared) by fin_s0 / fin_t
         if constexpr (W == FIN_S0) fin_s0(st, d1);
         else if constexpr (W == FIN_V) fin_v(st, d1);

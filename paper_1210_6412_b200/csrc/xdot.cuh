@@ -1574,6 +1574,11 @@ __global__ void __launch_bounds__(xd::NT) k_xdot(xd::Args A, SolveState* st) {
     if (W != SQ_TEST && st->stop) return;  // stopped earlier in this iteration (uniform)
     double d[2];
     if (!xd::xdot_body(A, d)) return;
+    if (W != SQ_TEST && st->sharded) {  // the exchange point finishes (k_finalize)
+        st->xd[0] = d[0];
+        st->xd[1] = d[1];
+        return;
+    }
     if constexpr (W == SQ_S0) fin_s0(st, d[0]);
     else if constexpr (W == SQ_V) fin_v(st, d[0]);
     else if constexpr (W == SQ_T) fin_t(st, d[0], d[1]);

@@ -196,6 +196,16 @@ class ShardMatrix:
             self._L.mcr_matrix_destroy(self._h)
             self._h = None
 
+    def set_dots(self, dots: str = "sequential", dot_blocks: int = 1) -> None:
+        """BiCGStab's inner products on this shard (mcr_set_dot_mode / mcr_set_dot_blocks):
+        "sequential" -- the reference's left-to-right sums of the whole gathered vectors, the same
+        bits on every rank and as one GPU; "tree" -- per-rank trees combined in rank order."""
+        rc = self._L.mcr_set_dot_mode(self._h, _lib.DOT_MODES[dots])
+        if rc == _lib.MCR_OK:
+            rc = self._L.mcr_set_dot_blocks(self._h, int(dot_blocks))
+        if rc != _lib.MCR_OK:
+            _raise_native(rc)
+
     def solve(self, method: str, b_local, x0_local, tol: float, max_it: int):
         fn = {"jacobi": self._L.mcr_jacobi, "bicgstab": self._L.mcr_bicgstab}[method]
         b = np.ascontiguousarray(b_local, dtype=np.float64)
@@ -223,6 +233,10 @@ def _guess_slice(shard: ShardMatrix, cfg) -> Optional[np.ndarray]:
 def _solve_sharded(method, shard: ShardMatrix, b_local, config, raise_errors=True):
     cfg = config or SolverConfig()
     start = time.perf_counter()
+    if method == "bicgstab":  # the reference's dot order by default (solvers.py:136-141, 384-396)
+        dots = getattr(cfg, "dot_products", "sequential")
+        blocks = cfg.resolved_workers() if getattr(cfg, "parallel_dot_products", False) else 1
+        shard.set_dots("tree" if dots == "tree" else "sequential", max(1, int(blocks)))
     rc, x, rep = shard.solve(method, b_local, _guess_slice(shard, cfg), cfg.tolerance,
                              cfg.max_iterations)
     result, err = outcome(rc, x, rep, start)

@@ -411,18 +411,19 @@ def _solve_parallel(method: str, m, b, config) -> SolveResult:
     if m.n == 0:
         return _empty_result(start)
     dots = getattr(cfg, "dot_products", "sequential")
-    if method == "bicgstab" and dots != "tree":
-        # the reference's inner products (solvers.py:384-396): one left-to-right chain over
-        # all rows, or with parallel_dot_products one chain per _row_blocks block of
-        # resolved_workers() blocks, block results added in order -- on one GPU
-        blocks = cfg.resolved_workers() if getattr(cfg, "parallel_dot_products", False) else 1
+    blocks = cfg.resolved_workers() if getattr(cfg, "parallel_dot_products", False) else 1
+    if method == "bicgstab" and dots == "serial":  # the one-CTA check mode: one GPU
         return _solve(method, m, b, cfg, dots=dots, dot_blocks=max(1, int(blocks)))
+    # BiCGStab's inner products (solvers.py:384-396) on row shards: every rank sums the whole
+    # gathered vectors left to right (one chain, or with parallel_dot_products one chain per
+    # _row_blocks block of resolved_workers() blocks, combined in order) -- the same bits as
+    # the reference and as one GPU (dist._solve_sharded)
     devices = parallel_devices(int(m.n), cfg)
     from .dist import shard_rows, solve_local_group
     while len(devices) > 1 and shard_rows(int(m.n), len(devices), len(devices) - 1)[1] < 1:
         devices = devices[:-1]  # ceil(n/k) blocks: every shard must hold rows
     if len(devices) == 1:
-        return _solve(method, m, b, cfg, device=devices[0])
+        return _solve(method, m, b, cfg, device=devices[0], dot_blocks=max(1, int(blocks)))
     result, _ = solve_local_group(method, m, b, len(devices), cfg, devices=devices)
     return SolveResult(result.x, result.iterations, result.converged, result.residual_inf,
                        time.perf_counter() - start)

@@ -4,8 +4,10 @@
 row block (global columns) with mcr_shard_create and runs the same multi-rank driver a
 torchrun/NCCL job runs, with the collectives as event-ordered device copies. Bar, as for
 the reference's own row-block parallel solvers (T/test_solvers.py:157-172, 242-256):
-Jacobi bit-identical to the reference at every world size (x, iterations, residual);
-BiCGStab (the row-sharded tree mode: dots reduced per rank, then in rank order) within the
+Jacobi and BiCGStab bit-identical to the reference at every world size (x, iterations,
+residual): the sharded BiCGStab gathers the vectors of each inner product and every rank sums
+the whole vectors in the reference's order (k_xdot), so all ranks take the reference's scalar
+steps. The opt-in tree order (per-rank trees combined in rank order) is checked within the
 north-star tolerance.
 The NCCL transport itself is exercised at world size 1 (one GPU per box here).
 """
@@ -28,7 +30,7 @@ def mods():
     return dist, solvers
 
 
-def run(mods, method, name, world, p2p=False):
+def run(mods, method, name, world, p2p=False, dots="sequential"):
     dist, gs = mods
     m, b = system(name)
     if dist.shard_rows(m.n, world, world - 1)[1] < 1:
@@ -36,7 +38,7 @@ def run(mods, method, name, world, p2p=False):
     exp = expected(name, method)
     c = exp["config"]
     conf = gs.SolverConfig(tolerance=c["tolerance"], max_iterations=c["max_iterations"],
-                           guess_seed=c["guess_seed"])
+                           guess_seed=c["guess_seed"], dot_products=dots)
     try:
         res, per = dist.solve_local_group(method, m, b, world, conf, p2p=p2p)
         return exp, "ok", res, None, per
@@ -53,8 +55,8 @@ def rel_err(x, ref):
     return float(np.max(np.abs(x - ref))) / scale if len(ref) else 0.0
 
 
-def check(mods, method, name, world, iter_slack=1, p2p=False):
-    exp, outcome, res, err, per = run(mods, method, name, world, p2p)
+def check(mods, method, name, world, iter_slack=1, p2p=False, dots="sequential"):
+    exp, outcome, res, err, per = run(mods, method, name, world, p2p, dots)
     assert outcome == exp["outcome"], (name, world, outcome, exp["outcome"])
     if outcome == "zero_diagonal":
         assert err.index == exp["zero_index"]
@@ -68,7 +70,7 @@ def check(mods, method, name, world, iter_slack=1, p2p=False):
     if outcome == "breakdown":
         assert err.which == exp["which"]
         assert err.iteration == exp["breakdown_iteration"]
-    if method == "jacobi":
+    if method == "jacobi" or dots == "sequential":
         assert res.iterations == exp["iterations"], (name, world, res.iterations, exp["iterations"])
         assert np.array_equal(got_x, ref_x), (name, world, rel_err(got_x, ref_x))
         assert sha(res.x) == exp["x_sha256"]
@@ -99,6 +101,14 @@ def test_sharded_bicgstab_matches_reference(mods, name, world):
     check(mods, "bicgstab", name, world)
 
 
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("name", ["c1_seed77", "c4_2000_3999", "crit3_1281", "parallel_large"])
+def test_sharded_bicgstab_tree_order(mods, name, world):
+    """The opt-in tree order on shards: x within the north-star tolerance; its stopping
+    iteration may move with the order (c2 below)."""
+    check(mods, "bicgstab", name, world, iter_slack=3, dots="tree")
+
+
 @pytest.mark.parametrize("name", KATS)
 @pytest.mark.parametrize("method", ["jacobi", "bicgstab"])
 def test_sharded_known_answers(mods, name, method):
@@ -111,7 +121,7 @@ def test_sharded_world_one_equals_single_gpu(mods):
     dist, gs = mods
     m, b = system("c1_trial0")
     r1, _ = dist.solve_local_group("bicgstab", m, b, 1)
-    r0 = gs.DeviceMatrix(m, 0, 5).solve("bicgstab", b, None, 1e-10, 10_000, dots="tree")  # TILES_STREAM
+    r0 = gs.DeviceMatrix(m, 0, 5).solve("bicgstab", b, None, 1e-10, 10_000)  # TILES_STREAM
     assert r0[0] == 0 and r1.iterations == r0[2].iterations
     assert np.array_equal(r1.x, r0[1])
 
@@ -119,12 +129,12 @@ def test_sharded_world_one_equals_single_gpu(mods):
 @pytest.mark.slow
 @pytest.mark.parametrize("world", [2, 4])
 def test_sharded_c2(mods, world):
-    """Jacobi bit-identical. BiCGStab: at C2 the stopping iteration moves with ANY change of
-    the inner-product summation order (reference cumsum 79, exactly rounded fsum 83, BLAS dot
-    84: tools/bicgstab_sensitivity.py); per-rank partials summed in rank order land at 85 for
-    world 2 and 4, x within 1e-9 of the reference."""
+    """Jacobi and BiCGStab bit-identical (BiCGStab stops at the reference's 79). In the opt-in
+    tree order the stopping iteration moves (reference cumsum 79, exactly rounded fsum 83, BLAS
+    dot 84: tools/bicgstab_sensitivity.py; rank-order partials land at 85), x within 1e-9."""
     check(mods, "jacobi", "c2_trial0", world)
-    check(mods, "bicgstab", "c2_trial0", world, iter_slack=6)
+    check(mods, "bicgstab", "c2_trial0", world)
+    check(mods, "bicgstab", "c2_trial0", world, iter_slack=6, dots="tree")
 
 
 def test_shard_bounds_rejected(mods):
@@ -229,7 +239,7 @@ def test_sharded_staged_layout_in_use(mods, monkeypatch):
 
 def test_fused_p2p_c2(mods):
     check(mods, "jacobi", "c2_trial0", 4, p2p=True)
-    check(mods, "bicgstab", "c2_trial0", 4, iter_slack=6, p2p=True)
+    check(mods, "bicgstab", "c2_trial0", 4, p2p=True)
 
 
 # ---- the registry's row-sharded drop-ins (SOLVERS["jacobi-gpu-par" / "bicgstab-gpu-par"]),
@@ -272,8 +282,9 @@ def test_registry_parallel_methods(mods, method, name, devices, monkeypatch):
     if outcome == "breakdown":
         assert err.which == exp["which"] and err.iteration == exp["breakdown_iteration"]
     # bit-identical to the reference at every shard count: Jacobi's iterates do not depend on
-    # the row split, and bicgstab-gpu-par's default (reference-order) inner products run on
-    # one GPU, as the reference's bicgstab_solve_parallel is bit-identical to its sequential one
+    # the row split, and bicgstab-gpu-par's default (reference-order) inner products are summed
+    # over the gathered vectors on every shard, as the reference's bicgstab_solve_parallel is
+    # bit-identical to its sequential one
     assert res.iterations == exp["iterations"]
     assert np.array_equal(got_x, ref_x)
     assert float(res.residual_inf).hex() == exp["residual_inf"]
@@ -300,8 +311,8 @@ def test_registry_parallel_workers_clamped(mods, monkeypatch):
 
 
 def test_registry_parallel_sequential_dots_is_exact(mods, monkeypatch):
-    """bicgstab-gpu-par with the reference's sequential inner products runs the one-GPU exact
-    mode (one chain over all rows): bit-identical to the reference's bicgstab."""
+    """bicgstab-gpu-par with the reference's sequential inner products on two shards (one
+    chain over all gathered rows on each): bit-identical to the reference's bicgstab."""
     dist, gs = mods
     monkeypatch.setenv("MCR_GPU_DEVICES", "0,0")
     name = "c4_2000_3999"
@@ -313,3 +324,26 @@ def test_registry_parallel_sequential_dots_is_exact(mods, monkeypatch):
     got = gs.SOLVERS["bicgstab-gpu-par"](m, b, conf)
     assert got.iterations == exp["iterations"]
     assert sha(got.x) == exp["x_sha256"]
+
+
+@pytest.mark.parametrize("devices", ["0,0", "0,0,0"])
+@pytest.mark.parametrize("key", ["pardots/c1_seed77/w4", "pardots/c4_2000_3999/w2",
+                                 "pardots/c4_5647_11293/w16", "pardots/parallel_large/w4"])
+def test_registry_parallel_dot_products_on_shards(mods, key, devices, monkeypatch):
+    """parallel_dot_products=True with config.workers = k on row shards (the shard count is
+    independent of k): the k _row_blocks chains of the gathered vectors, combined in order --
+    the reference's bicgstab_solve_parallel bit for bit (golden_extra, made by the reference)."""
+    import json
+    import os
+    dist, gs = mods
+    here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    with open(os.path.join(here, "golden_extra.json")) as fh:
+        exp = json.load(fh)["cases"][key]
+    monkeypatch.setenv("MCR_GPU_DEVICES", devices)
+    m, b = system(key.split("/")[1])
+    res = gs.SOLVERS["bicgstab-gpu-par"](m, b, gs.SolverConfig(workers=exp["workers"],
+                                                               parallel_dot_products=True))
+    assert res.iterations == exp["iterations"], (key, devices, res.iterations)
+    assert sha(res.x) == exp["x_sha256"]
+    assert float(res.residual_inf).hex() == exp["residual_inf"]
+
