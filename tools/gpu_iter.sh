@@ -1,4 +1,5 @@
 cd $GRAFT_REPO_ROOT
-O=gpurun_out/r02q; mkdir -p $O
-timeout 1500 python -m pytest tests -m gpu -x -q > $O/pytest.log 2>&1; echo rc=$? >> $O/pytest.log
-MCR_GPU_DEVICES=0,0 timeout 600 python bench.py --gpus 2 --steps 3 --warmup 1 > $O/c2_2shards.json 2> $O/c2_2shards.err
+O=gpurun_out/r02s; mkdir -p $O
+timeout 900 python -m pytest tests/test_gpu_dots.py tests/test_gpu_parity.py -x -q > $O/pytest.log 2>&1; echo rc=$? >> $O/pytest.log
+timeout 300 python tools/time_c4.py > $O/c4.json 2> $O/c4.err
+timeout 300 python bench.py --config c1 --no-cpu-baseline > $O/c1.json 2> $O/c1.err
