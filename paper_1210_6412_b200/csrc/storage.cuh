@@ -289,21 +289,31 @@ int alloc_csr(mcr_matrix* h, int64_t n, int64_t nnz) {
 
 // Host -> device copies of pageable arrays (a reference CsrMatrix holds plain numpy arrays).
 // cudaMemcpyAsync from pageable memory stages through the driver's own pinned buffer with one
-// host thread; here H2D_THREADS threads each copy their share of the bytes through their own
+// host thread; here h2d_threads() threads each copy their share of the bytes through their own
 // ring of pinned chunks (host memcpy into chunk k while the DMA engine drains chunk k-1), so
 // the host-side copy runs in parallel and overlaps the transfer. Pinned sources and small
 // copies go straight to cudaMemcpyAsync. MCR_H2D_RING=0 turns the ring off.
 struct H2DPart { void* dst; const void* src; size_t bytes; };
-constexpr int H2D_THREADS = 8, H2D_SLOTS = 3;
+constexpr int H2D_MAX_THREADS = 32, H2D_SLOTS = 3;
 constexpr size_t H2D_CHUNK = 4u << 20, H2D_MIN = 8u << 20;
 
 struct H2DRing {
     std::mutex mu;
-    char* buf[H2D_THREADS][H2D_SLOTS] = {};
-    cudaEvent_t ev[H2D_THREADS][H2D_SLOTS] = {};
+    char* buf[H2D_MAX_THREADS][H2D_SLOTS] = {};
+    cudaEvent_t ev[H2D_MAX_THREADS][H2D_SLOTS] = {};
     bool ready = false, failed = false;
 };
 inline H2DRing& h2d_ring() { static H2DRing r; return r; }
+// host threads of the ring: MCR_H2D_THREADS, default 8 (clamped to the host's threads)
+inline int h2d_threads() {
+    static const int n = [] {
+        int t = 8;
+        if (const char* e = getenv("MCR_H2D_THREADS")) t = atoi(e);
+        const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+        return std::max(1, std::min({t, hw, H2D_MAX_THREADS}));
+    }();
+    return n;
+}
 
 inline bool host_pinned(const void* p) {
     cudaPointerAttributes a;
@@ -328,7 +338,7 @@ inline int h2d_copy(const std::vector<H2DPart>& parts, cudaStream_t stream) {
     H2DRing& R = h2d_ring();
     std::lock_guard<std::mutex> lock(R.mu);
     if (!R.ready && !R.failed) {
-        for (int t = 0; t < H2D_THREADS && !R.failed; ++t)
+        for (int t = 0; t < h2d_threads() && !R.failed; ++t)
             for (int s = 0; s < H2D_SLOTS; ++s) {
                 if (cudaHostAlloc((void**)&R.buf[t][s], H2D_CHUNK, cudaHostAllocPortable) != cudaSuccess ||
                     cudaEventCreateWithFlags(&R.ev[t][s], cudaEventDisableTiming) != cudaSuccess) {
@@ -345,7 +355,8 @@ inline int h2d_copy(const std::vector<H2DPart>& parts, cudaStream_t stream) {
         return MCR_OK;
     }
     // thread t copies bytes [t*share, (t+1)*share) of the concatenated parts
-    const size_t share = (total + H2D_THREADS - 1) / H2D_THREADS;
+    const int NTH = h2d_threads();
+    const size_t share = (total + NTH - 1) / NTH;
     std::atomic<int> err{cudaSuccess};
     int device = 0;
     CK(cudaGetDevice(&device));
@@ -371,7 +382,7 @@ inline int h2d_copy(const std::vector<H2DPart>& parts, cudaStream_t stream) {
         }
     };
     std::vector<std::thread> th;
-    for (int t = 1; t < H2D_THREADS; ++t) th.emplace_back(work, t);
+    for (int t = 1; t < NTH; ++t) th.emplace_back(work, t);
     work(0);
     for (auto& x : th) x.join();
     CK((cudaError_t)err.load());

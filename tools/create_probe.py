@@ -37,7 +37,7 @@ def child():
         if i >= 2:
             ts.append(dt)
     mb = (rs.nbytes + col.nbytes + val.nbytes) / 1e6
-    print(f"ring={os.environ.get('MCR_H2D_RING', '1')}: create {1e3 * min(ts):.2f} ms min, "
+    print(f"ring={os.environ.get('MCR_H2D_RING', '1')} threads={os.environ.get('MCR_H2D_THREADS', '8')}: create {1e3 * min(ts):.2f} ms min, "
           f"{1e3 * sum(ts) / len(ts):.2f} ms mean for {mb:.0f} MB ({mb / 1e3 / min(ts):.1f} GB/s)")
 
 
@@ -45,5 +45,6 @@ if __name__ == "__main__":
     if len(sys.argv) > 1:
         child()
     else:
-        for ring in ("0", "1"):
-            subprocess.run([sys.executable, __file__, "child"], env={**os.environ, "MCR_H2D_RING": ring})
+        for ring, th in (("0", "8"), ("1", "4"), ("1", "8"), ("1", "12"), ("1", "16")):
+            subprocess.run([sys.executable, __file__, "child"],
+                           env={**os.environ, "MCR_H2D_RING": ring, "MCR_H2D_THREADS": th})
