@@ -155,6 +155,18 @@ __device__ __forceinline__ unsigned long long gtime() {
 #define XT_MARK(t) do {} while (0)
 #define XT_ADD(S, k, t0) do {} while (0)
 #endif
+#ifdef MCR_XDOT_TRACE  // per-CTA phase timestamps of one launch, printed by the root (diagnostics)
+__device__ unsigned long long g_xt[4096][6];
+__device__ int g_xn;
+__device__ __forceinline__ unsigned long long xt_now() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define XTR(slot, k) do { if (threadIdx.x == 0) g_xt[(slot)][(k)] = xt_now(); } while (0)
+#else
+#define XTR(slot, k) do {} while (0)
+#endif
 
 // parity of D/u for a displacement D that is a multiple of u = ulp(binade e) (e >= RUN_MIN_E,
 // so a non-zero D is a normal number): the bit of D's significand that has weight u
@@ -423,6 +435,46 @@ __device__ __forceinline__ void sim_elems(const double* p, int cnt, double& v, d
     flush_range(amin, amax, lo, hi, km);
     if (has_b) flush_range(bmin, bmax, lo, hi, km);
     v = x;
+}
+
+// plain left-to-right sum of p[i0, i1) onto v (8 loads ahead of the add chain)
+__device__ __forceinline__ double walk_elems(const double* p, int i0, int i1, double v) {
+    int i = i0;
+    for (; i + 8 <= i1; i += 8) {
+        double x[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] = p[i + j];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v = dadd(v, x[j]);
+    }
+    const int r = i1 - i;  // 0..7 left: all loads first (a load per add would chain the latency)
+    double x[7];
+#pragma unroll
+    for (int j = 0; j < 7; ++j) x[j] = j < r ? p[i + j] : 0.0;
+#pragma unroll
+    for (int j = 0; j < 7; ++j)
+        if (j < r) v = dadd(v, x[j]);
+    return v;
+}
+
+// the same with the products addressed as a 32-bit shared-memory window offset (no generic ->
+// shared conversion per call: the walker runs this for every HARD segment)
+__device__ __forceinline__ double lds_f64(uint32_t a) {
+    double x;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(x) : "r"(a));
+    return x;
+}
+__device__ __forceinline__ double walk_elems_s(uint32_t p, int i0, int i1, double v) {
+    int i = i0;
+    for (; i + 8 <= i1; i += 8) {
+        double x[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] = lds_f64(p + 8u * (uint32_t)(i + j));
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v = dadd(v, x[j]);
+    }
+    for (; i < i1; ++i) v = dadd(v, lds_f64(p + 8u * (uint32_t)i));
+    return v;
 }
 
 // Per lane, no collectives: carry v through the thread runs [t0, t1) of the CTA range in shared
@@ -911,15 +963,22 @@ __device__ int build_cta(const Args& A, const Seq& q, int si, const Smem& M, dou
     __shared__ int s_tk;
     __shared__ double s_pred;
     XT_MARK(t_start);
+#ifdef MCR_XDOT_TRACE
+    const unsigned long long xt_entry = xt_now();
+#endif
     if (tid == 0) s_tk = (int)atomicAdd(S.ticket + si, 1u);
     __syncthreads();
     const int ci = s_tk;
     const int slot = q.cta0 + ci;
+#ifdef MCR_XDOT_TRACE
+    if (tid == 0) g_xt[slot][0] = xt_entry;
+#endif
     const long long c0 = q.a + (long long)ci * NT * E;
     const long long c1 = min(q.b, c0 + (long long)NT * E);
     const int len = (int)max(0ll, c1 - c0);
     const unsigned fl = load_products(q, c0, len, M.sp);
     XT_ADD(S, ST_T_LOAD, t_start);
+    XTR(slot, 1);
     XT_MARK(t_lb);
     if (A.upto == 1) return ci;
     double total;
@@ -944,10 +1003,12 @@ __device__ int build_cta(const Args& A, const Seq& q, int si, const Smem& M, dou
     __syncthreads();
     const double pred_cta = s_pred;
     XT_ADD(S, ST_T_LOOKBACK, t_lb);
+    XTR(slot, 2);
     XT_MARK(t_runs);
     if (A.upto == 2) return ci;
     runs_and_warp_pieces(S, q, c0, len, E, dadd(pred_cta, exc), fl, M, A.upto == 13, ci == 0);
     XT_ADD(S, ST_T_RUNS, t_runs);
+    XTR(slot, 3);
     XT_MARK(t_cta);
     if (A.upto == 3 || A.upto == 13) return ci;
     {  // the warp pieces, for the root's fallback (before the tree folds them in place)
@@ -968,7 +1029,39 @@ __device__ int build_cta(const Args& A, const Seq& q, int si, const Smem& M, dou
         for (int k = tid; k < (int)(sizeof(Desc) / 16); k += NT) dst[k] = src[k];
     }
     XT_ADD(S, ST_T_CTA, t_cta);
+    XTR(slot, 4);
     return ci;
+}
+
+// One lane: the true value v through piece D (shared memory), as piece_apply_r / table_eval
+// decide it but without the start-shift bookkeeping a carried table needs (the root walks the
+// exact value) and without shuffles: the entry is read straight from D.
+__device__ __forceinline__ bool exact_apply(const Desc* D, double& v) {
+    const Hdr& h = D->h;
+    if (h.kind == K_RUN) {
+        double lo = -INFINITY, hi = INFINITY;
+        int km = KM_NONE;
+        return run_apply(hdr_run(h), v, lo, hi, km);
+    }
+    const unsigned long long b = bt(v), mb = b & ~SGN;
+    const long long d = (long long)(mb - h.mb0);
+    const int k = (int)(d & 31);
+    const LaneS e = D->l[k];
+    const int kmh = D->kmh[k];
+    if ((kmh & 1) || (int)(b >> 63) != h.neg) return false;
+    if (d >= 0 && d < 32) {  // a candidate itself
+        v = e.out;
+        return true;
+    }
+    const unsigned long long cb = h.mb0 + (unsigned long long)k;
+    const int ce = dexp(cb), se = dexp(mb);
+    if (ce != se || se == 0 || se == 0x7ff) return false;
+    const double dl = dsub(v, fb(cb | ((unsigned long long)h.neg << 63)));  // exact
+    if (!(dl >= (double)e.lo && dl <= (double)e.hi)) return false;
+    const int sh = (kmh >> 1) - (ce - 1075);
+    if (sh > 5 && (sh >= 63 || ((d - k) & ((1ll << sh) - 1)))) return false;
+    v = dadd(e.out, dl);  // exact
+    return true;
 }
 
 // Warp 0 of the root: warp w's elements of CTA range ci from the exact start v: the 32
@@ -982,8 +1075,25 @@ __device__ double warp_walk_exact(const Args& A, const Seq& q, int ci, int w, do
     const long long w0 = c0 + (long long)w * 32 * E;
     const int wl = (int)max(0ll, min(c1 - w0, (long long)32 * E));
     double* sp = M.sp;  // the root's own range is no longer needed
-    for (int k = lane; k < wl; k += 32) sp[k] = dmul(__ldcg(q.u + w0 + k), __ldcg(q.v + w0 + k));
+#ifdef MCR_XDOT_TRACE
+    if (lane == 0 && g_xn < 60) { g_xt[4000 + g_xn][0] = 5; g_xt[4000 + g_xn][1] = 0; g_xt[4000 + g_xn++][2] = xt_now(); }
+#endif
+    for (int k0 = lane; k0 < wl; k0 += 32 * 8) {  // 8 pairs in flight per lane (one L2 round trip)
+        double a[8], b[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int k = k0 + 32 * j;
+            a[j] = k < wl ? __ldcg(q.u + w0 + k) : 0.0;
+            b[j] = k < wl ? __ldcg(q.v + w0 + k) : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (k0 + 32 * j < wl) sp[k0 + 32 * j] = dmul(a[j], b[j]);
+    }
     __syncwarp();
+#ifdef MCR_XDOT_TRACE
+    if (lane == 0 && g_xn < 60) { g_xt[4000 + g_xn][0] = 5; g_xt[4000 + g_xn][1] = 1; g_xt[4000 + g_xn++][2] = xt_now(); }
+#endif
     const int t0 = lane * E, tl = max(0, min(E, wl - t0));
     double ts = 0.0;
     for (int k = 0; k < tl; ++k) ts = dadd(ts, sp[t0 + k]);
@@ -1026,6 +1136,9 @@ __device__ double warp_walk_exact(const Args& A, const Seq& q, int ci, int w, do
             }
         }
     }
+#ifdef MCR_XDOT_TRACE
+    if (lane == 0 && g_xn < 60) { g_xt[4000 + g_xn][0] = 5; g_xt[4000 + g_xn][1] = 2; g_xt[4000 + g_xn++][2] = xt_now(); }
+#endif
     for (int t = 0; t < 32; ++t) {  // uniform: every lane carries the same value
         Run G;
 #pragma unroll
@@ -1041,73 +1154,10 @@ __device__ double warp_walk_exact(const Args& A, const Seq& q, int ci, int w, do
         if (run_apply(G, v, lo, hi, km)) continue;
         if (lane == 0) stat(A.S, ST_CHUNK_FB);
         const int b0 = t * E, bl = max(0, min(E, wl - b0));
-        for (int k = 0; k < bl; ++k) v = dadd(v, sp[b0 + k]);
+        v = walk_elems(sp + b0, 0, bl, v);  // loads ahead of the add chain
     }
     __syncwarp();
     return v;
-}
-
-// All threads of the root: CTA range ci from its true start (*s_v) through its warp pieces
-// (staged from global memory); a warp piece that does not apply is walked exactly.
-__device__ void walk_warps(const Args& A, const Seq& q, int ci, const Smem& M, double* s_v) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) stat(A.S, ST_CTA_FB);
-    __syncthreads();  // wd may still be read
-    {
-        const double2* src = (const double2*)(A.S.warp + (size_t)(q.cta0 + ci) * NW);
-        double2* dst = (double2*)M.wd;
-        for (int k = threadIdx.x; k < (int)(NW * sizeof(Desc) / 16); k += NT) dst[k] = __ldcg(src + k);
-    }
-    __syncthreads();
-    if (warp == 0) {
-        double v = *s_v;
-        for (int w = 0; w < NW; ++w) {
-            double lo = -INFINITY, hi = INFINITY;
-            int km = KM_NONE;
-            if (piece_apply_r(load_piece(M.wd + w), v, lo, hi, km)) continue;
-            if (lane == 0) stat(A.S, ST_WARP_FB);
-            v = warp_walk_exact(A, q, ci, w, v, M);
-        }
-        if (lane == 0) *s_v = v;
-    }
-    __syncthreads();
-}
-
-// All threads of the root: carry the true value (*s_v) through the staged CTA pieces
-// [c0, c1) (the stage holds pieces from index b0), rebuilding the ones it cannot use.
-__device__ void walk_ctas(const Args& A, const Seq& q, int b0, int c0, int c1, const Smem& M,
-                          double* s_red, double* s_v) {
-    __shared__ int s_c;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    int c = c0;
-    while (c < c1) {
-        __syncthreads();
-        if (warp == 0) {
-            double v = *s_v;
-            int cc = c;
-            for (; cc < c1; ++cc) {
-                const PieceR P = load_piece(M.stage + (cc - b0));
-                double lo = -INFINITY, hi = INFINITY;
-                int km = KM_NONE;
-#ifdef MCR_XDOT_DEBUG
-                const double v_in = v;
-#endif
-                if (!piece_apply_r(P, v, lo, hi, km)) {
-#ifdef MCR_XDOT_DEBUG
-                    why_failed(A.S, M.stage + (cc - b0), v_in);
-#endif
-                    break;
-                }
-            }
-            if (lane == 0) { *s_v = v; s_c = cc; }
-        }
-        __syncthreads();
-        c = s_c;
-        if (c >= c1) break;
-        walk_warps(A, q, c, M, s_v);
-        ++c;
-    }
-    __syncthreads();
 }
 
 // The last CTA of a sequence: the sequence's sum, from the exact start 0.0.
@@ -1118,6 +1168,7 @@ __device__ double root(const Args& A, const Seq& q, int si, const Smem& M, doubl
     __shared__ double s_v;
     __shared__ int s_nf, s_ok;
     XT_MARK(t_root);
+    XTR(4095, 0);
     if (threadIdx.x == 0) {
         s_nf = (int)((__ldcg((const int*)S.flags + si) >> 1) & 1);
         s_v = 0.0;
@@ -1187,6 +1238,7 @@ __device__ double root(const Args& A, const Seq& q, int si, const Smem& M, doubl
         __syncthreads();
         tree_fold(M, 0, A.E, M.td, false);
         XT_ADD(S, ST_T_ROOT_GROUPS, t_root);
+        XTR(4095, 1);
         XT_MARK(t_walk);
         if (warp == 0) {  // the whole batch from the true value
             double v = s_v, lo = -INFINITY, hi = INFINITY;
@@ -1198,25 +1250,68 @@ __device__ double root(const Args& A, const Seq& q, int si, const Smem& M, doubl
             }
         }
         __syncthreads();
-        if (!s_ok) {  // group by group; a group that does not apply, CTA piece by CTA piece
-            for (int g = 0; g < NW; ++g) {
-                const int g0 = b0 + g * Q, g1 = min(b1, g0 + Q);
-                if (g0 >= g1) break;
-                if (warp == 0) {
-                    double v = s_v, lo = -INFINITY, hi = INFINITY;
-                    int km = KM_NONE;
-                    const bool ok = piece_apply_r(load_piece(M.gd + g), v, lo, hi, km);
-                    if (lane == 0) {
-                        s_ok = ok;
-                        if (ok) s_v = v;
+        if (!s_ok) {
+            // warp 0 carries the true value group by group; a group that does not apply, CTA
+            // piece by CTA piece (staged); a CTA piece that does not, warp piece by warp piece
+            // (from global memory); a warp piece that does not, its thread runs rebuilt around
+            // the exact start. Lane 0 applies the pieces (exact_apply: no shuffles, no
+            // bookkeeping), the whole warp only loads and rebuilds.
+            if (warp == 0) {
+                double v = s_v;
+                for (int g = 0; g < NW; ++g) {
+                    const int g0 = b0 + g * Q, g1 = min(b1, g0 + Q);
+                    if (g0 >= g1) break;
+                    int ok = 0;
+                    if (lane == 0) ok = exact_apply(M.gd + g, v);
+                    ok = __shfl_sync(FULL, ok, 0);
+                    if (ok) continue;
+                    if (lane == 0) stat(S, ST_GROUP_FB);
+#ifdef MCR_XDOT_TRACE
+                    if (lane == 0 && g_xn < 60) { g_xt[4000 + g_xn][0] = 1; g_xt[4000 + g_xn][1] = g; g_xt[4000 + g_xn++][2] = xt_now(); }
+#endif
+                    for (int c = g0; c < g1; ++c) {
+                        if (lane == 0) ok = exact_apply(M.stage + (c - b0), v);
+                        ok = __shfl_sync(FULL, ok, 0);
+                        if (ok) continue;
+                        if (lane == 0) stat(S, ST_CTA_FB);
+#ifdef MCR_XDOT_TRACE
+                        if (lane == 0 && g_xn < 60) { g_xt[4000 + g_xn][0] = 2; g_xt[4000 + g_xn][1] = c; g_xt[4000 + g_xn++][2] = xt_now(); }
+#endif
+                        {  // this CTA range's warp pieces
+                            const double2* src = (const double2*)(S.warp + (size_t)(q.cta0 + c) * NW);
+                            double2* dst = (double2*)M.wd;
+                            constexpr int NV = (int)(NW * sizeof(Desc) / 16), PER = (NV + 31) / 32;
+                            __syncwarp();
+                            double2 t[PER];  // every load issued before the first store
+#pragma unroll
+                            for (int j = 0; j < PER; ++j) {
+                                const int k = lane + 32 * j;
+                                t[j] = k < NV ? __ldcg(src + k) : make_double2(0.0, 0.0);
+                            }
+#pragma unroll
+                            for (int j = 0; j < PER; ++j)
+                                if (lane + 32 * j < NV) dst[lane + 32 * j] = t[j];
+                            __syncwarp();
+                        }
+                        for (int w = 0; w < NW; ++w) {
+                            if (lane == 0) ok = exact_apply(M.wd + w, v);
+                            ok = __shfl_sync(FULL, ok, 0);
+                            if (ok) continue;
+                            if (lane == 0) stat(S, ST_WARP_FB);
+#ifdef MCR_XDOT_TRACE
+                            if (lane == 0 && g_xn < 60) { g_xt[4000 + g_xn][0] = 3; g_xt[4000 + g_xn][1] = w; g_xt[4000 + g_xn++][2] = xt_now(); }
+#endif
+                            v = __shfl_sync(FULL, v, 0);
+                            v = warp_walk_exact(A, q, c, w, v, M);
+#ifdef MCR_XDOT_TRACE
+                            if (lane == 0 && g_xn < 60) { g_xt[4000 + g_xn][0] = 4; g_xt[4000 + g_xn][1] = w; g_xt[4000 + g_xn++][2] = xt_now(); }
+#endif
+                        }
                     }
                 }
-                __syncthreads();
-                if (!s_ok) {
-                    if (threadIdx.x == 0) stat(S, ST_GROUP_FB);
-                    walk_ctas(A, q, b0, g0, g1, M, s_red, &s_v);
-                }
+                if (lane == 0) s_v = v;
             }
+            __syncthreads();
         }
         XT_ADD(S, ST_T_ROOT_WALK, t_walk);
         __syncthreads();
@@ -1224,6 +1319,24 @@ __device__ double root(const Args& A, const Seq& q, int si, const Smem& M, doubl
     // cumsum starts from p_0 itself: -0.0 survives only when every product is -0.0
     if (threadIdx.x == 0 && s_v == 0.0 && q.b > q.a && !(__ldcg((const int*)S.flags + si) & 1)) s_v = -0.0;
     if (threadIdx.x == 0) stat(S, ST_T_LAUNCHES);
+#ifdef MCR_XDOT_TRACE
+    XTR(4095, 2);
+    if (threadIdx.x == 0) {
+        unsigned long long t0 = ~0ull;
+        for (int c = 0; c < n; ++c) t0 = min(t0, g_xt[q.cta0 + c][0]);
+        for (int c = 0; c < n; ++c) {
+            const unsigned long long* g = g_xt[q.cta0 + c];
+            printf("xt cta %d: entry %.1f load %.1f lb %.1f runs %.1f cta %.1f\n", c, (g[0] - t0) * 1e-3,
+                   (g[1] - t0) * 1e-3, (g[2] - t0) * 1e-3, (g[3] - t0) * 1e-3, (g[4] - t0) * 1e-3);
+        }
+        printf("xt t0 %llu\n", t0);
+        for (int i = 0; i < g_xn; ++i)
+            printf("xt ev %llu %llu %.1f\n", g_xt[4000 + i][0], g_xt[4000 + i][1], (g_xt[4000 + i][2] - t0) * 1e-3);
+        g_xn = 0;
+        printf("xt root: start %.1f groups %.1f end %.1f\n", (g_xt[4095][0] - t0) * 1e-3,
+               (g_xt[4095][1] - t0) * 1e-3, (g_xt[4095][2] - t0) * 1e-3);
+    }
+#endif
     __syncthreads();
     return s_v;
 }
@@ -1382,46 +1495,6 @@ __device__ __forceinline__ double seg_step(const SegRun& R, double v, bool& ok) 
     const bool in = ng ? (vhi <= bot && vlo >= top) : (vlo >= bot && vhi <= top);
     ok = dexp(b) == R.e && ng == R.neg && in;
     return vn;
-}
-
-// plain left-to-right sum of p[i0, i1) onto v (8 loads ahead of the add chain)
-__device__ __forceinline__ double walk_elems(const double* p, int i0, int i1, double v) {
-    int i = i0;
-    for (; i + 8 <= i1; i += 8) {
-        double x[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) x[j] = p[i + j];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) v = dadd(v, x[j]);
-    }
-    const int r = i1 - i;  // 0..7 left: all loads first (a load per add would chain the latency)
-    double x[7];
-#pragma unroll
-    for (int j = 0; j < 7; ++j) x[j] = j < r ? p[i + j] : 0.0;
-#pragma unroll
-    for (int j = 0; j < 7; ++j)
-        if (j < r) v = dadd(v, x[j]);
-    return v;
-}
-
-// the same with the products addressed as a 32-bit shared-memory window offset (no generic ->
-// shared conversion per call: the walker runs this for every HARD segment)
-__device__ __forceinline__ double lds_f64(uint32_t a) {
-    double x;
-    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(x) : "r"(a));
-    return x;
-}
-__device__ __forceinline__ double walk_elems_s(uint32_t p, int i0, int i1, double v) {
-    int i = i0;
-    for (; i + 8 <= i1; i += 8) {
-        double x[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) x[j] = lds_f64(p + 8u * (uint32_t)(i + j));
-#pragma unroll
-        for (int j = 0; j < 8; ++j) v = dadd(v, x[j]);
-    }
-    for (; i < i1; ++i) v = dadd(v, lds_f64(p + 8u * (uint32_t)i));
-    return v;
 }
 
 constexpr int XS_SERIAL_MAX = 384;  // up to this many products one thread just adds them
