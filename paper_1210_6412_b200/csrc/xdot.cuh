@@ -502,8 +502,7 @@ __device__ void lane_walk_threads(const Run* s_runs, const double* sp, int len, 
         if (run_apply(R, v, lo, hi, km)) continue;
         const int b0 = t * E, bl = max(0, min(E, len - b0));
         if (bare) {  // the value only: this lane then serves its exact start alone
-#pragma unroll 4
-            for (int k = 0; k < bl; ++k) v = dadd(v, sp[b0 + k]);
+            v = walk_elems(sp + b0, 0, bl, v);
             lo = fmax(lo, 0.0);
             hi = fmin(hi, 0.0);
         } else if (R.e == E_HARD) {  // its sums change binade: the per-sum path straight away
@@ -953,6 +952,37 @@ __device__ void tree_fold(const Smem& M, int len, int E, Desc* p, bool walk) {
     }
 }
 
+// One lane: the true value v through piece D (shared memory), as piece_apply_r / table_eval
+// decide it but without the start-shift bookkeeping a carried table needs (the root walks the
+// exact value) and without shuffles: the entry is read straight from D.
+__device__ __forceinline__ bool exact_apply(const Desc* D, double& v) {
+    const Hdr& h = D->h;
+    if (h.kind == K_RUN) {
+        double lo = -INFINITY, hi = INFINITY;
+        int km = KM_NONE;
+        return run_apply(hdr_run(h), v, lo, hi, km);
+    }
+    const unsigned long long b = bt(v), mb = b & ~SGN;
+    const long long d = (long long)(mb - h.mb0);
+    const int k = (int)(d & 31);
+    const LaneS e = D->l[k];
+    const int kmh = D->kmh[k];
+    if ((kmh & 1) || (int)(b >> 63) != h.neg) return false;
+    if (d >= 0 && d < 32) {  // a candidate itself
+        v = e.out;
+        return true;
+    }
+    const unsigned long long cb = h.mb0 + (unsigned long long)k;
+    const int ce = dexp(cb), se = dexp(mb);
+    if (ce != se || se == 0 || se == 0x7ff) return false;
+    const double dl = dsub(v, fb(cb | ((unsigned long long)h.neg << 63)));  // exact
+    if (!(dl >= (double)e.lo && dl <= (double)e.hi)) return false;
+    const int sh = (kmh >> 1) - (ce - 1075);
+    if (sh > 5 && (sh >= 63 || ((d - k) & ((1ll << sh) - 1)))) return false;
+    v = dadd(e.out, dl);  // exact
+    return true;
+}
+
 // Phase 1 of every CTA: take a ticket (the CTA's place in the sequence), build the CTA piece
 // around the predicted start (the sum of the totals of the CTAs before it: look-back) and
 // publish it. Returns the ticket.
@@ -1017,7 +1047,36 @@ __device__ int build_cta(const Args& A, const Seq& q, int si, const Smem& M, dou
         for (int k = tid; k < (int)(NW * sizeof(Desc) / 16); k += NT) dst[k] = src[k];
     }
     __syncthreads();
-    tree_fold(M, len, E, M.wd, true);  // the CTA piece, in wd[0]
+    if (ci == 0 && A.upto != 13) {
+        // The sequence's first CTA starts at exactly 0.0, and the root evaluates its piece
+        // there alone: warp 0 carries that value through the warp pieces (a piece that does not
+        // apply: its threads, values only), and the CTA piece is that value at candidate 0.0
+        // (every other candidate a hole) -- no tree of tables, whose lanes would otherwise walk
+        // the stretches that do not compose with the slack bookkeeping.
+        const int lane = tid & 31;
+        if ((tid >> 5) == 0) {
+            double v = 0.0;
+            for (int w = 0; w < NW; ++w) {
+                int ok = 0;
+                if (lane == 0) ok = exact_apply(M.wd + w, v);
+                ok = __shfl_sync(FULL, ok, 0);
+                v = __shfl_sync(FULL, v, 0);
+                if (ok) continue;
+                double lo = 0.0, hi = 0.0;
+                int km = KM_NONE;
+                lane_walk_threads(M.runs, M.sp, len, E, w * 32, w * 32 + 32, v, lo, hi, km, nullptr, true);
+            }
+            __syncwarp();
+            LaneR L;
+            L.out = v; L.lo = 0.0; L.hi = 0.0; L.km = KM_NONE;
+            L.hole = (lane != 0 || dexp(bt(v)) == 0x7ff) ? 1 : 0;
+            store_lane(M.wd, lane, L);
+            if (lane == 0) hdr_set_table(M.wd->h, window_mb0(0.0), 0, 0.0);
+        }
+        __syncthreads();
+    } else {
+        tree_fold(M, len, E, M.wd, true);  // the CTA piece, in wd[0]
+    }
     if (S.stats && tid == 0 && M.wd[0].h.kind == K_TABLE) stat(S, ST_CTA_TABLE);
 #ifdef MCR_XDOT_DEBUG
     if ((tid >> 5) == 0 && M.wd[0].h.kind == K_TABLE)
@@ -1031,37 +1090,6 @@ __device__ int build_cta(const Args& A, const Seq& q, int si, const Smem& M, dou
     XT_ADD(S, ST_T_CTA, t_cta);
     XTR(slot, 4);
     return ci;
-}
-
-// One lane: the true value v through piece D (shared memory), as piece_apply_r / table_eval
-// decide it but without the start-shift bookkeeping a carried table needs (the root walks the
-// exact value) and without shuffles: the entry is read straight from D.
-__device__ __forceinline__ bool exact_apply(const Desc* D, double& v) {
-    const Hdr& h = D->h;
-    if (h.kind == K_RUN) {
-        double lo = -INFINITY, hi = INFINITY;
-        int km = KM_NONE;
-        return run_apply(hdr_run(h), v, lo, hi, km);
-    }
-    const unsigned long long b = bt(v), mb = b & ~SGN;
-    const long long d = (long long)(mb - h.mb0);
-    const int k = (int)(d & 31);
-    const LaneS e = D->l[k];
-    const int kmh = D->kmh[k];
-    if ((kmh & 1) || (int)(b >> 63) != h.neg) return false;
-    if (d >= 0 && d < 32) {  // a candidate itself
-        v = e.out;
-        return true;
-    }
-    const unsigned long long cb = h.mb0 + (unsigned long long)k;
-    const int ce = dexp(cb), se = dexp(mb);
-    if (ce != se || se == 0 || se == 0x7ff) return false;
-    const double dl = dsub(v, fb(cb | ((unsigned long long)h.neg << 63)));  // exact
-    if (!(dl >= (double)e.lo && dl <= (double)e.hi)) return false;
-    const int sh = (kmh >> 1) - (ce - 1075);
-    if (sh > 5 && (sh >= 63 || ((d - k) & ((1ll << sh) - 1)))) return false;
-    v = dadd(e.out, dl);  // exact
-    return true;
 }
 
 // Warp 0 of the root: warp w's elements of CTA range ci from the exact start v: the 32
