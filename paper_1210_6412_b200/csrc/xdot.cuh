@@ -155,18 +155,6 @@ __device__ __forceinline__ unsigned long long gtime() {
 #define XT_MARK(t) do {} while (0)
 #define XT_ADD(S, k, t0) do {} while (0)
 #endif
-#ifdef MCR_XDOT_TRACE  // per-CTA phase timestamps of one launch, printed by the root (diagnostics)
-__device__ unsigned long long g_xt[4096][6];
-__device__ int g_xn;
-__device__ __forceinline__ unsigned long long xt_now() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
-#define XTR(slot, k) do { if (threadIdx.x == 0) g_xt[(slot)][(k)] = xt_now(); } while (0)
-#else
-#define XTR(slot, k) do {} while (0)
-#endif
 
 // parity of D/u for a displacement D that is a multiple of u = ulp(binade e) (e >= RUN_MIN_E,
 // so a non-zero D is a normal number): the bit of D's significand that has weight u
@@ -454,26 +442,6 @@ __device__ __forceinline__ double walk_elems(const double* p, int i0, int i1, do
 #pragma unroll
     for (int j = 0; j < 7; ++j)
         if (j < r) v = dadd(v, x[j]);
-    return v;
-}
-
-// the same with the products addressed as a 32-bit shared-memory window offset (no generic ->
-// shared conversion per call: the walker runs this for every HARD segment)
-__device__ __forceinline__ double lds_f64(uint32_t a) {
-    double x;
-    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(x) : "r"(a));
-    return x;
-}
-__device__ __forceinline__ double walk_elems_s(uint32_t p, int i0, int i1, double v) {
-    int i = i0;
-    for (; i + 8 <= i1; i += 8) {
-        double x[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) x[j] = lds_f64(p + 8u * (uint32_t)(i + j));
-#pragma unroll
-        for (int j = 0; j < 8; ++j) v = dadd(v, x[j]);
-    }
-    for (; i < i1; ++i) v = dadd(v, lds_f64(p + 8u * (uint32_t)i));
     return v;
 }
 
@@ -993,22 +961,15 @@ __device__ int build_cta(const Args& A, const Seq& q, int si, const Smem& M, dou
     __shared__ int s_tk;
     __shared__ double s_pred;
     XT_MARK(t_start);
-#ifdef MCR_XDOT_TRACE
-    const unsigned long long xt_entry = xt_now();
-#endif
     if (tid == 0) s_tk = (int)atomicAdd(S.ticket + si, 1u);
     __syncthreads();
     const int ci = s_tk;
     const int slot = q.cta0 + ci;
-#ifdef MCR_XDOT_TRACE
-    if (tid == 0) g_xt[slot][0] = xt_entry;
-#endif
     const long long c0 = q.a + (long long)ci * NT * E;
     const long long c1 = min(q.b, c0 + (long long)NT * E);
     const int len = (int)max(0ll, c1 - c0);
     const unsigned fl = load_products(q, c0, len, M.sp);
     XT_ADD(S, ST_T_LOAD, t_start);
-    XTR(slot, 1);
     XT_MARK(t_lb);
     if (A.upto == 1) return ci;
     double total;
@@ -1033,12 +994,10 @@ __device__ int build_cta(const Args& A, const Seq& q, int si, const Smem& M, dou
     __syncthreads();
     const double pred_cta = s_pred;
     XT_ADD(S, ST_T_LOOKBACK, t_lb);
-    XTR(slot, 2);
     XT_MARK(t_runs);
     if (A.upto == 2) return ci;
     runs_and_warp_pieces(S, q, c0, len, E, dadd(pred_cta, exc), fl, M, A.upto == 13, ci == 0);
     XT_ADD(S, ST_T_RUNS, t_runs);
-    XTR(slot, 3);
     XT_MARK(t_cta);
     if (A.upto == 3 || A.upto == 13) return ci;
     {  // the warp pieces, for the root's fallback (before the tree folds them in place)
@@ -1088,7 +1047,6 @@ __device__ int build_cta(const Args& A, const Seq& q, int si, const Smem& M, dou
         for (int k = tid; k < (int)(sizeof(Desc) / 16); k += NT) dst[k] = src[k];
     }
     XT_ADD(S, ST_T_CTA, t_cta);
-    XTR(slot, 4);
     return ci;
 }
 
@@ -1103,25 +1061,8 @@ __device__ double warp_walk_exact(const Args& A, const Seq& q, int ci, int w, do
     const long long w0 = c0 + (long long)w * 32 * E;
     const int wl = (int)max(0ll, min(c1 - w0, (long long)32 * E));
     double* sp = M.sp;  // the root's own range is no longer needed
-#ifdef MCR_XDOT_TRACE
-    if (lane == 0 && g_xn < 60) { g_xt[4000 + g_xn][0] = 5; g_xt[4000 + g_xn][1] = 0; g_xt[4000 + g_xn++][2] = xt_now(); }
-#endif
-    for (int k0 = lane; k0 < wl; k0 += 32 * 8) {  // 8 pairs in flight per lane (one L2 round trip)
-        double a[8], b[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const int k = k0 + 32 * j;
-            a[j] = k < wl ? __ldcg(q.u + w0 + k) : 0.0;
-            b[j] = k < wl ? __ldcg(q.v + w0 + k) : 0.0;
-        }
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-            if (k0 + 32 * j < wl) sp[k0 + 32 * j] = dmul(a[j], b[j]);
-    }
+    for (int k = lane; k < wl; k += 32) sp[k] = dmul(__ldcg(q.u + w0 + k), __ldcg(q.v + w0 + k));
     __syncwarp();
-#ifdef MCR_XDOT_TRACE
-    if (lane == 0 && g_xn < 60) { g_xt[4000 + g_xn][0] = 5; g_xt[4000 + g_xn][1] = 1; g_xt[4000 + g_xn++][2] = xt_now(); }
-#endif
     const int t0 = lane * E, tl = max(0, min(E, wl - t0));
     double ts = 0.0;
     for (int k = 0; k < tl; ++k) ts = dadd(ts, sp[t0 + k]);
@@ -1164,9 +1105,6 @@ __device__ double warp_walk_exact(const Args& A, const Seq& q, int ci, int w, do
             }
         }
     }
-#ifdef MCR_XDOT_TRACE
-    if (lane == 0 && g_xn < 60) { g_xt[4000 + g_xn][0] = 5; g_xt[4000 + g_xn][1] = 2; g_xt[4000 + g_xn++][2] = xt_now(); }
-#endif
     for (int t = 0; t < 32; ++t) {  // uniform: every lane carries the same value
         Run G;
 #pragma unroll
@@ -1182,10 +1120,73 @@ __device__ double warp_walk_exact(const Args& A, const Seq& q, int ci, int w, do
         if (run_apply(G, v, lo, hi, km)) continue;
         if (lane == 0) stat(A.S, ST_CHUNK_FB);
         const int b0 = t * E, bl = max(0, min(E, wl - b0));
-        v = walk_elems(sp + b0, 0, bl, v);  // loads ahead of the add chain
+        for (int k = 0; k < bl; ++k) v = dadd(v, sp[b0 + k]);
     }
     __syncwarp();
     return v;
+}
+
+// All threads of the root: CTA range ci from its true start (*s_v) through its warp pieces
+// (staged from global memory); a warp piece that does not apply is walked exactly.
+__device__ void walk_warps(const Args& A, const Seq& q, int ci, const Smem& M, double* s_v) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) stat(A.S, ST_CTA_FB);
+    __syncthreads();  // wd may still be read
+    {
+        const double2* src = (const double2*)(A.S.warp + (size_t)(q.cta0 + ci) * NW);
+        double2* dst = (double2*)M.wd;
+        for (int k = threadIdx.x; k < (int)(NW * sizeof(Desc) / 16); k += NT) dst[k] = __ldcg(src + k);
+    }
+    __syncthreads();
+    if (warp == 0) {
+        double v = *s_v;
+        for (int w = 0; w < NW; ++w) {
+            double lo = -INFINITY, hi = INFINITY;
+            int km = KM_NONE;
+            if (piece_apply_r(load_piece(M.wd + w), v, lo, hi, km)) continue;
+            if (lane == 0) stat(A.S, ST_WARP_FB);
+            v = warp_walk_exact(A, q, ci, w, v, M);
+        }
+        if (lane == 0) *s_v = v;
+    }
+    __syncthreads();
+}
+
+// All threads of the root: carry the true value (*s_v) through the staged CTA pieces
+// [c0, c1) (the stage holds pieces from index b0), rebuilding the ones it cannot use.
+__device__ void walk_ctas(const Args& A, const Seq& q, int b0, int c0, int c1, const Smem& M,
+                          double* s_red, double* s_v) {
+    __shared__ int s_c;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int c = c0;
+    while (c < c1) {
+        __syncthreads();
+        if (warp == 0) {
+            double v = *s_v;
+            int cc = c;
+            for (; cc < c1; ++cc) {
+                const PieceR P = load_piece(M.stage + (cc - b0));
+                double lo = -INFINITY, hi = INFINITY;
+                int km = KM_NONE;
+#ifdef MCR_XDOT_DEBUG
+                const double v_in = v;
+#endif
+                if (!piece_apply_r(P, v, lo, hi, km)) {
+#ifdef MCR_XDOT_DEBUG
+                    why_failed(A.S, M.stage + (cc - b0), v_in);
+#endif
+                    break;
+                }
+            }
+            if (lane == 0) { *s_v = v; s_c = cc; }
+        }
+        __syncthreads();
+        c = s_c;
+        if (c >= c1) break;
+        walk_warps(A, q, c, M, s_v);
+        ++c;
+    }
+    __syncthreads();
 }
 
 // The last CTA of a sequence: the sequence's sum, from the exact start 0.0.
@@ -1196,7 +1197,6 @@ __device__ double root(const Args& A, const Seq& q, int si, const Smem& M, doubl
     __shared__ double s_v;
     __shared__ int s_nf, s_ok;
     XT_MARK(t_root);
-    XTR(4095, 0);
     if (threadIdx.x == 0) {
         s_nf = (int)((__ldcg((const int*)S.flags + si) >> 1) & 1);
         s_v = 0.0;
@@ -1266,7 +1266,6 @@ __device__ double root(const Args& A, const Seq& q, int si, const Smem& M, doubl
         __syncthreads();
         tree_fold(M, 0, A.E, M.td, false);
         XT_ADD(S, ST_T_ROOT_GROUPS, t_root);
-        XTR(4095, 1);
         XT_MARK(t_walk);
         if (warp == 0) {  // the whole batch from the true value
             double v = s_v, lo = -INFINITY, hi = INFINITY;
@@ -1278,68 +1277,25 @@ __device__ double root(const Args& A, const Seq& q, int si, const Smem& M, doubl
             }
         }
         __syncthreads();
-        if (!s_ok) {
-            // warp 0 carries the true value group by group; a group that does not apply, CTA
-            // piece by CTA piece (staged); a CTA piece that does not, warp piece by warp piece
-            // (from global memory); a warp piece that does not, its thread runs rebuilt around
-            // the exact start. Lane 0 applies the pieces (exact_apply: no shuffles, no
-            // bookkeeping), the whole warp only loads and rebuilds.
-            if (warp == 0) {
-                double v = s_v;
-                for (int g = 0; g < NW; ++g) {
-                    const int g0 = b0 + g * Q, g1 = min(b1, g0 + Q);
-                    if (g0 >= g1) break;
-                    int ok = 0;
-                    if (lane == 0) ok = exact_apply(M.gd + g, v);
-                    ok = __shfl_sync(FULL, ok, 0);
-                    if (ok) continue;
-                    if (lane == 0) stat(S, ST_GROUP_FB);
-#ifdef MCR_XDOT_TRACE
-                    if (lane == 0 && g_xn < 60) { g_xt[4000 + g_xn][0] = 1; g_xt[4000 + g_xn][1] = g; g_xt[4000 + g_xn++][2] = xt_now(); }
-#endif
-                    for (int c = g0; c < g1; ++c) {
-                        if (lane == 0) ok = exact_apply(M.stage + (c - b0), v);
-                        ok = __shfl_sync(FULL, ok, 0);
-                        if (ok) continue;
-                        if (lane == 0) stat(S, ST_CTA_FB);
-#ifdef MCR_XDOT_TRACE
-                        if (lane == 0 && g_xn < 60) { g_xt[4000 + g_xn][0] = 2; g_xt[4000 + g_xn][1] = c; g_xt[4000 + g_xn++][2] = xt_now(); }
-#endif
-                        {  // this CTA range's warp pieces
-                            const double2* src = (const double2*)(S.warp + (size_t)(q.cta0 + c) * NW);
-                            double2* dst = (double2*)M.wd;
-                            constexpr int NV = (int)(NW * sizeof(Desc) / 16), PER = (NV + 31) / 32;
-                            __syncwarp();
-                            double2 t[PER];  // every load issued before the first store
-#pragma unroll
-                            for (int j = 0; j < PER; ++j) {
-                                const int k = lane + 32 * j;
-                                t[j] = k < NV ? __ldcg(src + k) : make_double2(0.0, 0.0);
-                            }
-#pragma unroll
-                            for (int j = 0; j < PER; ++j)
-                                if (lane + 32 * j < NV) dst[lane + 32 * j] = t[j];
-                            __syncwarp();
-                        }
-                        for (int w = 0; w < NW; ++w) {
-                            if (lane == 0) ok = exact_apply(M.wd + w, v);
-                            ok = __shfl_sync(FULL, ok, 0);
-                            if (ok) continue;
-                            if (lane == 0) stat(S, ST_WARP_FB);
-#ifdef MCR_XDOT_TRACE
-                            if (lane == 0 && g_xn < 60) { g_xt[4000 + g_xn][0] = 3; g_xt[4000 + g_xn][1] = w; g_xt[4000 + g_xn++][2] = xt_now(); }
-#endif
-                            v = __shfl_sync(FULL, v, 0);
-                            v = warp_walk_exact(A, q, c, w, v, M);
-#ifdef MCR_XDOT_TRACE
-                            if (lane == 0 && g_xn < 60) { g_xt[4000 + g_xn][0] = 4; g_xt[4000 + g_xn][1] = w; g_xt[4000 + g_xn++][2] = xt_now(); }
-#endif
-                        }
+        if (!s_ok) {  // group by group; a group that does not apply, CTA piece by CTA piece
+            for (int g = 0; g < NW; ++g) {
+                const int g0 = b0 + g * Q, g1 = min(b1, g0 + Q);
+                if (g0 >= g1) break;
+                if (warp == 0) {
+                    double v = s_v, lo = -INFINITY, hi = INFINITY;
+                    int km = KM_NONE;
+                    const bool ok = piece_apply_r(load_piece(M.gd + g), v, lo, hi, km);
+                    if (lane == 0) {
+                        s_ok = ok;
+                        if (ok) s_v = v;
                     }
                 }
-                if (lane == 0) s_v = v;
+                __syncthreads();
+                if (!s_ok) {
+                    if (threadIdx.x == 0) stat(S, ST_GROUP_FB);
+                    walk_ctas(A, q, b0, g0, g1, M, s_red, &s_v);
+                }
             }
-            __syncthreads();
         }
         XT_ADD(S, ST_T_ROOT_WALK, t_walk);
         __syncthreads();
@@ -1347,24 +1303,6 @@ __device__ double root(const Args& A, const Seq& q, int si, const Smem& M, doubl
     // cumsum starts from p_0 itself: -0.0 survives only when every product is -0.0
     if (threadIdx.x == 0 && s_v == 0.0 && q.b > q.a && !(__ldcg((const int*)S.flags + si) & 1)) s_v = -0.0;
     if (threadIdx.x == 0) stat(S, ST_T_LAUNCHES);
-#ifdef MCR_XDOT_TRACE
-    XTR(4095, 2);
-    if (threadIdx.x == 0) {
-        unsigned long long t0 = ~0ull;
-        for (int c = 0; c < n; ++c) t0 = min(t0, g_xt[q.cta0 + c][0]);
-        for (int c = 0; c < n; ++c) {
-            const unsigned long long* g = g_xt[q.cta0 + c];
-            printf("xt cta %d: entry %.1f load %.1f lb %.1f runs %.1f cta %.1f\n", c, (g[0] - t0) * 1e-3,
-                   (g[1] - t0) * 1e-3, (g[2] - t0) * 1e-3, (g[3] - t0) * 1e-3, (g[4] - t0) * 1e-3);
-        }
-        printf("xt t0 %llu\n", t0);
-        for (int i = 0; i < g_xn; ++i)
-            printf("xt ev %llu %llu %.1f\n", g_xt[4000 + i][0], g_xt[4000 + i][1], (g_xt[4000 + i][2] - t0) * 1e-3);
-        g_xn = 0;
-        printf("xt root: start %.1f groups %.1f end %.1f\n", (g_xt[4095][0] - t0) * 1e-3,
-               (g_xt[4095][1] - t0) * 1e-3, (g_xt[4095][2] - t0) * 1e-3);
-    }
-#endif
     __syncthreads();
     return s_v;
 }
@@ -1627,54 +1565,40 @@ __device__ void cta_seqdots(const double* buf, int n, CtaDots<NTH, K>& D, double
             for (int k = 0; k < K; ++k) {
                 if (k != warp) continue;
                 const double* p = buf + (size_t)k * n;
-                const uint32_t ps = smem_u32(p);
                 double v = 0.0;
-                // products to add one by one are collected into one pending stretch [w0, w1)
-                // (consecutive HARD segments, failed runs, warps of short segments) and added
-                // when a run is about to apply
-                int w0 = 0, w1 = 0;
                 for (int w = 0; w < NWS; ++w) {
                     const int cnt = D.cnt[k][w];
                     const SegRun* sg = &D.seg[k][w * 32];
 #ifdef MCR_XS_TIMING
                     nseg += cnt;
 #endif
-                    const int we0 = w * 32 * E, we1 = min(n, (w + 1) * 32 * E);
-                    if (cnt * 32 > we1 - we0) {  // a segment costs about 32 adds: many short ones, all one by one
-                        if (w1 != we0) { v = walk_elems_s(ps, w0, w1, v); w0 = we0; }
-                        w1 = max(w1, we1);
+                    // a warp of many short segments: its products one by one are cheaper
+                    if (cnt * 4 > min(n, (w + 1) * 32 * E) - w * 32 * E) {
+                        v = walk_elems(p, w * 32 * E, min(n, (w + 1) * 32 * E), v);
 #ifdef MCR_XS_TIMING
-                        nwalk += max(0, we1 - we0);
+                        nwalk += min(n, (w + 1) * 32 * E) - w * 32 * E;
 #endif
                         continue;
                     }
+                    // the next segment is loaded while this one is applied (its shared-memory
+                    // latency stays off the value's dependency chain); a HARD segment (e = 0)
+                    // never matches the exponent of a value that a run could apply to
                     SegRun cur = sg[0];
                     for (int j = 0; j < cnt; ++j) {
                         const SegRun nxt = sg[min(j + 1, cnt - 1)];
-                        if (cur.e == E_HARD) {
-                            if (w1 != cur.i0) { v = walk_elems_s(ps, w0, w1, v); w0 = cur.i0; }
-                            w1 = cur.i1;
+                        bool ok;
+                        const double vn = seg_step(cur, v, ok);
+                        if (ok && cur.e != E_HARD) {
+                            v = vn;
+                        } else {
+                            v = walk_elems(p, cur.i0, cur.i1, v);
 #ifdef MCR_XS_TIMING
                             nwalk += cur.i1 - cur.i0;
 #endif
-                        } else {
-                            if (w1 > w0) v = walk_elems_s(ps, w0, w1, v);
-                            w0 = w1 = cur.i1;
-                            bool ok;
-                            const double vn = seg_step(cur, v, ok);
-                            if (ok) {
-                                v = vn;
-                            } else {
-                                w0 = cur.i0;
-#ifdef MCR_XS_TIMING
-                                nwalk += cur.i1 - cur.i0;
-#endif
-                            }
                         }
                         cur = nxt;
                     }
                 }
-                if (w1 > w0) v = walk_elems_s(ps, w0, w1, v);
                 // cumsum starts from p_0 itself: -0.0 survives only when every product is -0.0
                 if (v == 0.0 && !(flags[k] & 1u)) v = -0.0;
                 D.out[k] = v;
@@ -1709,11 +1633,6 @@ __global__ void __launch_bounds__(xd::NT) k_xdot(xd::Args A, SolveState* st) {
     if (W != SQ_TEST && st->stop) return;  // stopped earlier in this iteration (uniform)
     double d[2];
     if (!xd::xdot_body(A, d)) return;
-    if (W != SQ_TEST && st->sharded) {  // the exchange point finishes (k_finalize)
-        st->xd[0] = d[0];
-        st->xd[1] = d[1];
-        return;
-    }
     if constexpr (W == SQ_S0) fin_s0(st, d[0]);
     else if constexpr (W == SQ_V) fin_v(st, d[0]);
     else if constexpr (W == SQ_T) fin_t(st, d[0], d[1]);
