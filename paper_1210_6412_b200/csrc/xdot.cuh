@@ -1195,7 +1195,7 @@ __device__ double root(const Args& A, const Seq& q, int si, const Smem& M, doubl
     const Scratch& S = A.S;
     const int n = q.ncta;
     __shared__ double s_v;
-    __shared__ int s_nf, s_ok;
+    __shared__ int s_nf;
     XT_MARK(t_root);
     if (threadIdx.x == 0) {
         s_nf = (int)((__ldcg((const int*)S.flags + si) >> 1) & 1);
@@ -1259,43 +1259,37 @@ __device__ double root(const Args& A, const Seq& q, int si, const Smem& M, doubl
                 hdr_set_run(G->h, run_empty(), 0.0);  // identity
             }
             __syncwarp();
-            const double2* src = (const double2*)G;
-            double2* dst = (double2*)(M.td + warp);
-            for (int k = lane; k < (int)(sizeof(Desc) / 16); k += 32) dst[k] = src[k];
         }
         __syncthreads();
-        tree_fold(M, 0, A.E, M.td, false);
         XT_ADD(S, ST_T_ROOT_GROUPS, t_root);
         XT_MARK(t_walk);
-        if (warp == 0) {  // the whole batch from the true value
-            double v = s_v, lo = -INFINITY, hi = INFINITY;
-            int km = KM_NONE;
-            const bool ok = piece_apply_r(load_piece(M.td), v, lo, hi, km);
-            if (lane == 0) {
-                s_ok = ok;
-                if (ok) s_v = v;
-            }
-        }
-        __syncthreads();
-        if (!s_ok) {  // group by group; a group that does not apply, CTA piece by CTA piece
-            for (int g = 0; g < NW; ++g) {
-                const int g0 = b0 + g * Q, g1 = min(b1, g0 + Q);
-                if (g0 >= g1) break;
-                if (warp == 0) {
-                    double v = s_v, lo = -INFINITY, hi = INFINITY;
-                    int km = KM_NONE;
-                    const bool ok = piece_apply_r(load_piece(M.gd + g), v, lo, hi, km);
-                    if (lane == 0) {
-                        s_ok = ok;
-                        if (ok) s_v = v;
-                    }
+        // Lane 0 of warp 0 carries the true value through the group tables until one does not
+        // apply (no tree over them: their windows already sit at the predictions, and a table
+        // application is cheaper than a tree level); a group that does not apply is walked CTA
+        // piece by CTA piece by the whole CTA (walk_ctas), then the walk resumes after it.
+        __shared__ int s_g;
+        const int ngroups = min(NW, (b1 - b0 + Q - 1) / Q);
+        for (int g = 0; g < ngroups;) {
+            if (warp == 0) {
+                double v = s_v;
+                int gg = g, ok = 1;
+                for (; gg < ngroups; ++gg) {
+                    if (lane == 0) ok = exact_apply(M.gd + gg, v);
+                    ok = __shfl_sync(FULL, ok, 0);
+                    if (!ok) break;
                 }
-                __syncthreads();
-                if (!s_ok) {
-                    if (threadIdx.x == 0) stat(S, ST_GROUP_FB);
-                    walk_ctas(A, q, b0, g0, g1, M, s_red, &s_v);
+                if (lane == 0) {
+                    s_v = v;
+                    s_g = gg;
                 }
             }
+            __syncthreads();
+            g = s_g;
+            if (g >= ngroups) break;
+            if (threadIdx.x == 0) stat(S, ST_GROUP_FB);
+            const int g0 = b0 + g * Q, g1 = min(b1, g0 + Q);
+            walk_ctas(A, q, b0, g0, g1, M, s_red, &s_v);
+            ++g;
         }
         XT_ADD(S, ST_T_ROOT_WALK, t_walk);
         __syncthreads();
