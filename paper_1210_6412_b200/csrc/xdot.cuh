@@ -1274,8 +1274,9 @@ __device__ double root(const Args& A, const Seq& q, int si, const Smem& M, doubl
                 double v = s_v;
                 int gg = g, ok = 1;
                 for (; gg < ngroups; ++gg) {
-                    if (lane == 0) ok = exact_apply(M.gd + gg, v);
-                    ok = __shfl_sync(FULL, ok, 0);
+                    double lo = -INFINITY, hi = INFINITY;
+                    int km = KM_NONE;
+                    ok = piece_apply_r(load_piece(M.gd + gg), v, lo, hi, km);  // uniform over the warp
                     if (!ok) break;
                 }
                 if (lane == 0) {
