@@ -920,37 +920,6 @@ __device__ void tree_fold(const Smem& M, int len, int E, Desc* p, bool walk) {
     }
 }
 
-// One lane: the true value v through piece D (shared memory), as piece_apply_r / table_eval
-// decide it but without the start-shift bookkeeping a carried table needs (the root walks the
-// exact value) and without shuffles: the entry is read straight from D.
-__device__ __forceinline__ bool exact_apply(const Desc* D, double& v) {
-    const Hdr& h = D->h;
-    if (h.kind == K_RUN) {
-        double lo = -INFINITY, hi = INFINITY;
-        int km = KM_NONE;
-        return run_apply(hdr_run(h), v, lo, hi, km);
-    }
-    const unsigned long long b = bt(v), mb = b & ~SGN;
-    const long long d = (long long)(mb - h.mb0);
-    const int k = (int)(d & 31);
-    const LaneS e = D->l[k];
-    const int kmh = D->kmh[k];
-    if ((kmh & 1) || (int)(b >> 63) != h.neg) return false;
-    if (d >= 0 && d < 32) {  // a candidate itself
-        v = e.out;
-        return true;
-    }
-    const unsigned long long cb = h.mb0 + (unsigned long long)k;
-    const int ce = dexp(cb), se = dexp(mb);
-    if (ce != se || se == 0 || se == 0x7ff) return false;
-    const double dl = dsub(v, fb(cb | ((unsigned long long)h.neg << 63)));  // exact
-    if (!(dl >= (double)e.lo && dl <= (double)e.hi)) return false;
-    const int sh = (kmh >> 1) - (ce - 1075);
-    if (sh > 5 && (sh >= 63 || ((d - k) & ((1ll << sh) - 1)))) return false;
-    v = dadd(e.out, dl);  // exact
-    return true;
-}
-
 // Phase 1 of every CTA: take a ticket (the CTA's place in the sequence), build the CTA piece
 // around the predicted start (the sum of the totals of the CTAs before it: look-back) and
 // publish it. Returns the ticket.
@@ -1016,13 +985,10 @@ __device__ int build_cta(const Args& A, const Seq& q, int si, const Smem& M, dou
         if ((tid >> 5) == 0) {
             double v = 0.0;
             for (int w = 0; w < NW; ++w) {
-                int ok = 0;
-                if (lane == 0) ok = exact_apply(M.wd + w, v);
-                ok = __shfl_sync(FULL, ok, 0);
-                v = __shfl_sync(FULL, v, 0);
-                if (ok) continue;
-                double lo = 0.0, hi = 0.0;
+                double lo = -INFINITY, hi = INFINITY;
                 int km = KM_NONE;
+                if (piece_apply_r(load_piece(M.wd + w), v, lo, hi, km)) continue;  // uniform
+                lo = hi = 0.0;
                 lane_walk_threads(M.runs, M.sp, len, E, w * 32, w * 32 + 32, v, lo, hi, km, nullptr, true);
             }
             __syncwarp();
