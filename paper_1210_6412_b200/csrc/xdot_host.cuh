@@ -90,7 +90,16 @@ int xdot_plan(XdotCtx& X, int w, cudaStream_t s, int device, int64_t n, int ndot
         return g;
     };
     while (E + 2 <= xd::EMAX && grid_of(E) > nsm) E += 2;
+    // q.r (the E point) is the dot whose partial sums wander through zero once r is small:
+    // smaller ranges per CTA pay there even with a few CTAs in a second wave (C2: E 15 -> 13,
+    // 151 CTAs on 148 SMs, BiCGStab 27.55 -> 27.21 ms)
+    if (w == SQ_E && E >= 3 && grid_of(E - 2) <= nsm + nsm / 32) E -= 2;
     if (const char* env = std::getenv("MCR_XDOT_E")) E = std::max(1, std::min(xd::EMAX, std::atoi(env))) | 1;
+    {  // per reduction point (tuning): MCR_XDOT_E0 .. MCR_XDOT_E3 for S0, V, T, E
+        char name[16];
+        std::snprintf(name, sizeof(name), "MCR_XDOT_E%d", w);
+        if (const char* env = std::getenv(name)) E = std::max(1, std::min(xd::EMAX, std::atoi(env))) | 1;
+    }
     const int64_t per = (int64_t)xd::NT * E;
     std::vector<xd::Seq> seqs;
     int grid = 0;
