@@ -46,7 +46,10 @@
 namespace mcr {
 namespace xd {
 
-constexpr int NT = 512;
+#ifndef XD_NT
+#define XD_NT 256  // threads per CTA (C2 BiCGStab: 512 -> 27.3 ms, 256 -> 25.2 ms, 128 -> 32.8 ms)
+#endif
+constexpr int NT = XD_NT;
 constexpr int NW = NT / 32;
 constexpr int EMAX = 31;
 constexpr unsigned long long MANT = 0x000FFFFFFFFFFFFFull;
@@ -1424,6 +1427,26 @@ __device__ __forceinline__ double seg_step(const SegRun& R, double v, bool& ok) 
     return vn;
 }
 
+// the same with the products addressed as a 32-bit shared-memory window offset (no generic ->
+// shared conversion per call: the walker runs this for every HARD segment)
+__device__ __forceinline__ double lds_f64(uint32_t a) {
+    double x;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(x) : "r"(a));
+    return x;
+}
+__device__ __forceinline__ double walk_elems_s(uint32_t p, int i0, int i1, double v) {
+    int i = i0;
+    for (; i + 8 <= i1; i += 8) {
+        double x[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] = lds_f64(p + 8u * (uint32_t)(i + j));
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v = dadd(v, x[j]);
+    }
+    for (; i < i1; ++i) v = dadd(v, lds_f64(p + 8u * (uint32_t)i));
+    return v;
+}
+
 constexpr int XS_SERIAL_MAX = 384;  // up to this many products one thread just adds them
 
 template <int NTH, int K>
@@ -1525,19 +1548,24 @@ __device__ void cta_seqdots(const double* buf, int n, CtaDots<NTH, K>& D, double
 #pragma unroll
             for (int k = 0; k < K; ++k) {
                 if (k != warp) continue;
-                const double* p = buf + (size_t)k * n;
+                const uint32_t ps = smem_u32(buf + (size_t)k * n);
                 double v = 0.0;
+                // products to add one by one are collected into one pending stretch [w0, w1)
+                // (consecutive HARD segments, failed runs, warps of short segments) and added
+                // when a run is about to apply
+                int w0 = 0, w1 = 0;
                 for (int w = 0; w < NWS; ++w) {
                     const int cnt = D.cnt[k][w];
                     const SegRun* sg = &D.seg[k][w * 32];
 #ifdef MCR_XS_TIMING
                     nseg += cnt;
 #endif
-                    // a warp of many short segments: its products one by one are cheaper
-                    if (cnt * 4 > min(n, (w + 1) * 32 * E) - w * 32 * E) {
-                        v = walk_elems(p, w * 32 * E, min(n, (w + 1) * 32 * E), v);
+                    const int we0 = w * 32 * E, we1 = min(n, (w + 1) * 32 * E);
+                    if (cnt * 32 > we1 - we0) {  // a segment costs about 32 adds: many short ones, all one by one
+                        if (w1 != we0) { v = walk_elems_s(ps, w0, w1, v); w0 = we0; }
+                        w1 = max(w1, we1);
 #ifdef MCR_XS_TIMING
-                        nwalk += min(n, (w + 1) * 32 * E) - w * 32 * E;
+                        nwalk += max(0, we1 - we0);
 #endif
                         continue;
                     }
@@ -1547,19 +1575,30 @@ __device__ void cta_seqdots(const double* buf, int n, CtaDots<NTH, K>& D, double
                     SegRun cur = sg[0];
                     for (int j = 0; j < cnt; ++j) {
                         const SegRun nxt = sg[min(j + 1, cnt - 1)];
-                        bool ok;
-                        const double vn = seg_step(cur, v, ok);
-                        if (ok && cur.e != E_HARD) {
-                            v = vn;
-                        } else {
-                            v = walk_elems(p, cur.i0, cur.i1, v);
+                        if (cur.e == E_HARD) {
+                            if (w1 != cur.i0) { v = walk_elems_s(ps, w0, w1, v); w0 = cur.i0; }
+                            w1 = cur.i1;
 #ifdef MCR_XS_TIMING
                             nwalk += cur.i1 - cur.i0;
 #endif
+                        } else {
+                            if (w1 > w0) v = walk_elems_s(ps, w0, w1, v);
+                            w0 = w1 = cur.i1;
+                            bool ok;
+                            const double vn = seg_step(cur, v, ok);
+                            if (ok) {
+                                v = vn;
+                            } else {
+                                w0 = cur.i0;
+#ifdef MCR_XS_TIMING
+                                nwalk += cur.i1 - cur.i0;
+#endif
+                            }
                         }
                         cur = nxt;
                     }
                 }
+                if (w1 > w0) v = walk_elems_s(ps, w0, w1, v);
                 // cumsum starts from p_0 itself: -0.0 survives only when every product is -0.0
                 if (v == 0.0 && !(flags[k] & 1u)) v = -0.0;
                 D.out[k] = v;
@@ -1594,6 +1633,11 @@ __global__ void __launch_bounds__(xd::NT) k_xdot(xd::Args A, SolveState* st) {
     if (W != SQ_TEST && st->stop) return;  // stopped earlier in this iteration (uniform)
     double d[2];
     if (!xd::xdot_body(A, d)) return;
+    if (W != SQ_TEST && st->sharded) {  // the exchange point finishes (k_finalize)
+        st->xd[0] = d[0];
+        st->xd[1] = d[1];
+        return;
+    }
     if constexpr (W == SQ_S0) fin_s0(st, d[0]);
     else if constexpr (W == SQ_V) fin_v(st, d[0]);
     else if constexpr (W == SQ_T) fin_t(st, d[0], d[1]);
