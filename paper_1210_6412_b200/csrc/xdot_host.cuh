@@ -50,6 +50,28 @@ inline int xdot_smem_max() {
     return v;
 }
 
+// resident k_xdot CTAs per SM the plans are sized for (MCR_XDOT_CPS, tuning; default 1) and the
+// dynamic shared memory each may then use
+inline int xdot_cps() {
+    static int v = 0;
+    if (!v) {
+        const char* env = std::getenv("MCR_XDOT_CPS");
+        v = env ? std::max(1, std::min(4, std::atoi(env))) : 1;
+    }
+    return v;
+}
+inline size_t xdot_smem_budget() {
+    const int cps = xdot_cps();
+    if (cps == 1) return (size_t)xdot_smem_max();
+    int dev = 0, per_sm = 228 * 1024, rsv = 1024, optin = 227 * 1024;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    cudaDeviceGetAttribute(&rsv, cudaDevAttrReservedSharedMemoryPerBlock, dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    const int stat_bytes = optin - 256 - xdot_smem_max();
+    return (size_t)std::min(xdot_smem_max(), per_sm / cps - rsv - stat_bytes - 256);
+}
+
 inline int sm_count(int device) {
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
@@ -77,7 +99,7 @@ int xdot_plan(XdotCtx& X, int w, cudaStream_t s, int device, int64_t n, int ndot
     const int nb = std::max(1, nblocks);
     std::vector<int64_t> lo, hi;
     row_blocks(n, nb, lo, hi);
-    const int nsm = sm_count(device);
+    const int nsm = sm_count(device) * xdot_cps();  // CTA slots
     const int64_t total = (int64_t)ndot * n;
     // one CTA per SM (the shared memory is sized for that): the smallest odd E whose grid fits
     int64_t E = (total + (int64_t)xd::NT * nsm - 1) / ((int64_t)xd::NT * nsm);
@@ -162,7 +184,9 @@ int xdot_plan(XdotCtx& X, int w, cudaStream_t s, int device, int64_t n, int ndot
     // the root stages its sequence's CTA pieces in shared memory (in batches if they do not fit)
     int maxc = 1;
     for (const auto& q : seqs) maxc = std::max(maxc, q.ncta);
-    const int room = (int)(((size_t)xdot_smem_max() - xd::smem_bytes((int)E, 0)) / sizeof(xd::Desc));
+    size_t budget = xdot_smem_budget();
+    if (budget < xd::smem_bytes((int)E, 1)) budget = (size_t)xdot_smem_max();  // E too large for the cap
+    const int room = (int)((budget - xd::smem_bytes((int)E, 0)) / sizeof(xd::Desc));
     P.stage = std::max(1, std::min(maxc, room));
     P.smem = xd::smem_bytes((int)E, P.stage);
     P.n = n;
