@@ -112,10 +112,11 @@ int xdot_plan(XdotCtx& X, int w, cudaStream_t s, int device, int64_t n, int ndot
         return g;
     };
     while (E + 2 <= xd::EMAX && grid_of(E) > nsm) E += 2;
-    // q.r (the E point) is the dot whose partial sums wander through zero once r is small:
-    // smaller ranges per CTA pay there even with a few CTAs in a second wave (C2: E 15 -> 13,
-    // 151 CTAs on 148 SMs, BiCGStab 27.55 -> 27.21 ms)
-    if (w == SQ_E && E >= 3 && grid_of(E - 2) <= nsm + nsm / 32) E -= 2;
+    // q.v and q.r (the V and E points): one step smaller ranges per CTA pay even with a few
+    // CTAs in a second wave (C2, 256 threads: V 27 -> 25, 157 CTAs on 148 SMs, BiCGStab
+    // 24.73 -> 24.38 ms; E 27 -> 25 neutral; a bigger second wave, E 23: 28.4 ms). The T point
+    // (two dots) fills the SMs at E = 53 (31: 25.32 ms, 45: 25.45, 63: 28.27).
+    if ((w == SQ_E || w == SQ_V) && E >= 3 && grid_of(E - 2) <= nsm + nsm / 16) E -= 2;
     if (const char* env = std::getenv("MCR_XDOT_E")) E = std::max(1, std::min(xd::EMAX, std::atoi(env))) | 1;
     {  // per reduction point (tuning): MCR_XDOT_E0 .. MCR_XDOT_E3 for S0, V, T, E
         char name[16];
