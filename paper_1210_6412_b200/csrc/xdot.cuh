@@ -987,10 +987,13 @@ __device__ int build_cta(const Args& A, const Seq& q, int si, const Smem& M, dou
         const int lane = tid & 31;
         if ((tid >> 5) == 0) {
             double v = 0.0;
+            PieceR P = load_piece(M.wd);
             for (int w = 0; w < NW; ++w) {
+                const PieceR Pc = P;
+                P = load_piece(M.wd + min(w + 1, NW - 1));  // next piece's loads off the chain
                 double lo = -INFINITY, hi = INFINITY;
                 int km = KM_NONE;
-                if (piece_apply_r(load_piece(M.wd + w), v, lo, hi, km)) continue;  // uniform
+                if (piece_apply_r(Pc, v, lo, hi, km)) continue;  // uniform
                 lo = hi = 0.0;
                 lane_walk_threads(M.runs, M.sp, len, E, w * 32, w * 32 + 32, v, lo, hi, km, nullptr, true);
             }
@@ -1109,10 +1112,13 @@ __device__ void walk_warps(const Args& A, const Seq& q, int ci, const Smem& M, d
     __syncthreads();
     if (warp == 0) {
         double v = *s_v;
+        PieceR P = load_piece(M.wd);
         for (int w = 0; w < NW; ++w) {
+            const PieceR Pc = P;
+            P = load_piece(M.wd + min(w + 1, NW - 1));  // next piece's loads off the chain
             double lo = -INFINITY, hi = INFINITY;
             int km = KM_NONE;
-            if (piece_apply_r(load_piece(M.wd + w), v, lo, hi, km)) continue;
+            if (piece_apply_r(Pc, v, lo, hi, km)) continue;
             if (lane == 0) stat(A.S, ST_WARP_FB);
             v = warp_walk_exact(A, q, ci, w, v, M);
         }
@@ -1133,8 +1139,9 @@ __device__ void walk_ctas(const Args& A, const Seq& q, int b0, int c0, int c1, c
         if (warp == 0) {
             double v = *s_v;
             int cc = c;
+            PieceR P = load_piece(M.stage + (cc - b0));
             for (; cc < c1; ++cc) {
-                const PieceR P = load_piece(M.stage + (cc - b0));
+                const PieceR Pn = load_piece(M.stage + (min(cc + 1, c1 - 1) - b0));
                 double lo = -INFINITY, hi = INFINITY;
                 int km = KM_NONE;
 #ifdef MCR_XDOT_DEBUG
@@ -1146,6 +1153,7 @@ __device__ void walk_ctas(const Args& A, const Seq& q, int b0, int c0, int c1, c
 #endif
                     break;
                 }
+                P = Pn;
             }
             if (lane == 0) { *s_v = v; s_c = cc; }
         }
@@ -1215,7 +1223,14 @@ __device__ double root(const Args& A, const Seq& q, int si, const Smem& M, doubl
                 const int gn = window_neg(gp);
                 double v = cand(mb0, gn, lane), lo = -INFINITY, hi = INFINITY;
                 int km = KM_NONE, hole = 0;
-                for (int c = g0; c < g1; ++c) hole |= piece_apply_r(load_piece(M.stage + (c - b0)), v, lo, hi, km) ? 0 : 1;
+                // the next piece is read from shared memory while this one applies (its load
+                // latency stays off the value's dependency chain)
+                PieceR P = load_piece(M.stage + (g0 - b0));
+                for (int c = g0; c < g1; ++c) {
+                    const PieceR Pn = load_piece(M.stage + (min(c + 1, g1 - 1) - b0));
+                    hole |= piece_apply_r(P, v, lo, hi, km) ? 0 : 1;
+                    P = Pn;
+                }
                 LaneR Lx;
                 Lx.out = v; Lx.lo = lo; Lx.hi = hi; Lx.km = km;
                 Lx.hole = (hole || dexp(bt(v)) == 0x7ff) ? 1 : 0;
@@ -1242,11 +1257,14 @@ __device__ double root(const Args& A, const Seq& q, int si, const Smem& M, doubl
             if (warp == 0) {
                 double v = s_v;
                 int gg = g, ok = 1;
+                PieceR P = load_piece(M.gd + gg);
                 for (; gg < ngroups; ++gg) {
+                    const PieceR Pn = load_piece(M.gd + min(gg + 1, ngroups - 1));
                     double lo = -INFINITY, hi = INFINITY;
                     int km = KM_NONE;
-                    ok = piece_apply_r(load_piece(M.gd + gg), v, lo, hi, km);  // uniform over the warp
+                    ok = piece_apply_r(P, v, lo, hi, km);  // uniform over the warp
                     if (!ok) break;
+                    P = Pn;
                 }
                 if (lane == 0) {
                     s_v = v;
