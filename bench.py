@@ -425,7 +425,7 @@ def run_ours(args):
         e2e_total = float(t.item())
     e2e_value = 2.0 * world * args.steps / e2e_total
     e2e_iters = {"jacobi": int(rj_e.iterations), "bicgstab": int(rb_e.iterations)}
-    h2d = 8 * (n + 1) + 8 * nnz + 8 * nnz + 2 * 8 * n
+    h2d = 8 * (n + 1) + 8 * nnz + 4 * nnz + 2 * 8 * n  # columns cross PCIe as int32 (narrowed on the host)
     d2h = 2 * 8 * n
 
     # the same through the device handle API with pinned host buffers (sub-record)

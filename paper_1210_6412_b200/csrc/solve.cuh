@@ -375,6 +375,7 @@ int jacobi_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double tol
 int bicgstab_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double tol,
                   int64_t max_it, double* d_x_out, mcr_report* rep) {
     NvtxRange range(h->sharded() ? "mcr.bicgstab.shard" : "mcr.bicgstab");
+    Trace tr;
     TRY(ensure_work(h));
     TRY(prepare_inputs(h, d_b, d_x0, V_X));
     Vecs V = base_vecs(h);
@@ -397,6 +398,7 @@ int bicgstab_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double t
     // the device, and takes over from the next iteration on; for small systems capture +
     // instantiation cost more than the batch hides, so they keep the host-batched loop.
     TRY(xdot_prepare(h, V));
+    tr.mark("bicgstab: dot plans ready");
     // the captured body depends on the dot mode (and the block plan): rebuild when it changed
     const long long gkey = (long long)h->seqdots * 1000003ll + h->dot_blocks;
     if (h->gl_bicg.key != gkey) {
@@ -483,7 +485,9 @@ int bicgstab_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double t
         iters += k;
         if (late_graph) {  // host work while the batch runs
             late_graph = false;
+            tr.mark("bicgstab: first batch issued");
             TRY(build_graph_loop(h, h->gl_bicg, GRAPH_UNROLL_BICG, body));
+            tr.mark("bicgstab: graph built");
             TRY(read_state(h));
             if (h->gl_bicg.exec && !h->h_st->stop && iters < max_it) {
                 const long long it0 = h->h_st->it;
@@ -502,6 +506,7 @@ int bicgstab_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double t
         TRY(read_state(h));
         batch = std::min(batch * 2, 32);
     }
+    tr.mark("bicgstab: loop returned");
     if (sh) TRY(allgather_full(h, h->vec(V_X)));  // this rank's x is its slice of V_X
     TRY(residual_into_state(h, h->vec(V_X), &launched));
     CK(cudaEventRecord(h->ev1, h->stream));
@@ -512,6 +517,7 @@ int bicgstab_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double t
         CK(cudaMemcpyAsync(d_x_out, V.x, sizeof(double) * (size_t)h->n, cudaMemcpyDeviceToDevice,
                            h->stream));
     CK(cudaStreamSynchronize(h->stream));
+    tr.mark("bicgstab: done");
     const SolveState& s = *h->h_st;
     rep->residual_inf = s.resid;
     rep->device_seconds = ms * 1e-3;

@@ -293,7 +293,22 @@ int alloc_csr(mcr_matrix* h, int64_t n, int64_t nnz) {
 // ring of pinned chunks (host memcpy into chunk k while the DMA engine drains chunk k-1), so
 // the host-side copy runs in parallel and overlaps the transfer. Pinned sources and small
 // copies go straight to cudaMemcpyAsync. MCR_H2D_RING=0 turns the ring off.
-struct H2DPart { void* dst; const void* src; size_t bytes; };
+// conv = 1: the source holds int64 values sent as int32 (the column indices: half the bytes
+// over PCIe), narrowed on the host while they are copied into the pinned chunks; their min /
+// max come back for the caller's range check.
+struct H2DPart { void* dst; const void* src; size_t bytes; int conv = 0; };
+
+inline void narrow_i64(int* out, const long long* in, size_t cnt, long long& mn, long long& mx) {
+    long long a = mn, b = mx;
+    for (size_t i = 0; i < cnt; ++i) {
+        const long long c = in[i];
+        a = c < a ? c : a;
+        b = c > b ? c : b;
+        out[i] = (int)c;
+    }
+    mn = a;
+    mx = b;
+}
 constexpr int H2D_MAX_THREADS = 32, H2D_SLOTS = 3;
 constexpr size_t H2D_CHUNK = 4u << 20, H2D_MIN = 8u << 20;
 
@@ -321,14 +336,29 @@ inline bool host_pinned(const void* p) {
     return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeManaged;
 }
 
-inline int h2d_copy(const std::vector<H2DPart>& parts, cudaStream_t stream) {
+inline bool h2d_ring_on() {
     static const bool on = [] { const char* e = getenv("MCR_H2D_RING"); return !e || atoi(e) != 0; }();
+    return on;
+}
+
+// Narrowing parts that cannot take the ring: converted into a host buffer, copied synchronously.
+inline int h2d_narrow_plain(const H2DPart& p, cudaStream_t stream, long long* cmin, long long* cmax) {
+    std::vector<int> tmp(p.bytes / 8);
+    narrow_i64(tmp.data(), (const long long*)p.src, tmp.size(), *cmin, *cmax);
+    CK(cudaMemcpyAsync(p.dst, tmp.data(), p.bytes / 2, cudaMemcpyHostToDevice, stream));
+    CK(cudaStreamSynchronize(stream));
+    return MCR_OK;
+}
+
+inline int h2d_copy(const std::vector<H2DPart>& parts, cudaStream_t stream, long long* cmin = nullptr,
+                    long long* cmax = nullptr) {
     std::vector<H2DPart> ring;
     size_t total = 0;
     for (const H2DPart& p : parts) {
         if (!p.bytes) continue;
-        if (!on || p.bytes < H2D_MIN || host_pinned(p.src)) {
-            CK(cudaMemcpyAsync(p.dst, p.src, p.bytes, cudaMemcpyHostToDevice, stream));
+        if (!h2d_ring_on() || p.bytes < H2D_MIN || host_pinned(p.src)) {
+            if (p.conv) TRY(h2d_narrow_plain(p, stream, cmin, cmax));
+            else CK(cudaMemcpyAsync(p.dst, p.src, p.bytes, cudaMemcpyHostToDevice, stream));
         } else {
             ring.push_back(p);
             total += p.bytes;
@@ -350,13 +380,17 @@ inline int h2d_copy(const std::vector<H2DPart>& parts, cudaStream_t stream) {
         R.ready = !R.failed;
     }
     if (!R.ready) {  // no pinned memory to be had: the driver's own staging
-        for (const H2DPart& p : ring)
-            CK(cudaMemcpyAsync(p.dst, p.src, p.bytes, cudaMemcpyHostToDevice, stream));
+        for (const H2DPart& p : ring) {
+            if (p.conv) TRY(h2d_narrow_plain(p, stream, cmin, cmax));
+            else CK(cudaMemcpyAsync(p.dst, p.src, p.bytes, cudaMemcpyHostToDevice, stream));
+        }
         return MCR_OK;
     }
-    // thread t copies bytes [t*share, (t+1)*share) of the concatenated parts
+    // thread t copies bytes [t*share, (t+1)*share) of the concatenated parts (whole 8-byte
+    // elements: every part is an array of them)
     const int NTH = h2d_threads();
-    const size_t share = (total + NTH - 1) / NTH;
+    const size_t share = ((total + NTH - 1) / NTH + 7) & ~(size_t)7;
+    std::vector<long long> tmin(NTH, LLONG_MAX), tmax(NTH, LLONG_MIN);
     std::atomic<int> err{cudaSuccess};
     int device = 0;
     CK(cudaGetDevice(&device));
@@ -369,7 +403,12 @@ inline int h2d_copy(const std::vector<H2DPart>& parts, cudaStream_t stream) {
             for (size_t o = a; o < b; o += H2D_CHUNK) {
                 const size_t len = std::min(H2D_CHUNK, b - o);
                 cudaError_t e = cudaEventSynchronize(R.ev[t][slot]);  // the slot's last DMA drained
-                if (e == cudaSuccess) {
+                if (e == cudaSuccess && p.conv) {
+                    narrow_i64((int*)R.buf[t][slot], (const long long*)((const char*)p.src + (o - base)),
+                               len / 8, tmin[t], tmax[t]);
+                    e = cudaMemcpyAsync((char*)p.dst + (o - base) / 2, R.buf[t][slot], len / 2,
+                                        cudaMemcpyHostToDevice, stream);
+                } else if (e == cudaSuccess) {
                     memcpy(R.buf[t][slot], (const char*)p.src + (o - base), len);
                     e = cudaMemcpyAsync((char*)p.dst + (o - base), R.buf[t][slot], len,
                                         cudaMemcpyHostToDevice, stream);
@@ -386,6 +425,11 @@ inline int h2d_copy(const std::vector<H2DPart>& parts, cudaStream_t stream) {
     work(0);
     for (auto& x : th) x.join();
     CK((cudaError_t)err.load());
+    if (cmin && cmax)
+        for (int t = 0; t < NTH; ++t) {
+            *cmin = std::min(*cmin, tmin[t]);
+            *cmax = std::max(*cmax, tmax[t]);
+        }
     return MCR_OK;
 }
 
@@ -398,38 +442,56 @@ int create_impl(mcr_matrix* h, int64_t n, const int64_t* rs, const int64_t* col,
     tr.mark("create: handle");
     const int64_t nnz = rs[n];
     TRY(alloc_csr(h, n, nnz));
-    // int64 columns -> int32 on the device, range-checked, then the row-order check. (A host
-    // conversion sending half the bytes was measured slower: the host threads compete with
-    // the value copy for host memory bandwidth.)
+    // int64 columns -> int32, range-checked, then the row-order check on the device. Pageable
+    // columns (a reference CsrMatrix) are narrowed on the host while the ring copies them, so
+    // half their bytes cross PCIe: the upload is bound by the link (≈27 GB/s on the test boxes;
+    // 4, 8, 12 and 16 ring threads measure the same), and C2's 184 MB become 144 MB (create
+    // 6.2-6.4 -> 5.5-5.7 ms, tools/dropin_probe.py). Pinned columns go over as they are and a
+    // kernel narrows them. MCR_HOST_NARROW=0: the kernel always.
+    static const bool narrow_env = [] { const char* e = getenv("MCR_HOST_NARROW"); return !e || atoi(e) != 0; }();
+    const bool host_narrow = narrow_env && nnz > 0 && h2d_ring_on() &&
+                             sizeof(long long) * (size_t)nnz >= H2D_MIN && !host_pinned(col);
     long long* tmp = nullptr;
     int* bad = nullptr;
-    CK(cudaMallocAsync((void**)&tmp, sizeof(long long) * (size_t)std::max<int64_t>(nnz, 1),
-                       h->stream));
+    if (!host_narrow)
+        CK(cudaMallocAsync((void**)&tmp, sizeof(long long) * (size_t)std::max<int64_t>(nnz, 1),
+                           h->stream));
     CK(cudaMallocAsync((void**)&bad, 2 * sizeof(int), h->stream));
     CK(cudaMemsetAsync(bad, 0, 2 * sizeof(int), h->stream));
     // the row tiles are cut on a host thread while the copies run
     bool monotone = true;
-    long long max_row = 0;
+    long long max_row = 0, cmin = LLONG_MAX, cmax = LLONG_MIN;
     std::vector<int> tiles;
-    std::thread cut([&] { tiles = make_tiles(n, rs, &max_row, &monotone); });
-    const int copied = h2d_copy({{h->rp, rs, sizeof(long long) * (size_t)(n + 1)},
-                                 {h->val, val, sizeof(double) * (size_t)nnz},
-                                 {tmp, col, sizeof(long long) * (size_t)nnz}}, h->stream);
+    std::thread cut([&] {
+        tiles = make_tiles(n, rs, &max_row, &monotone);
+        tr.mark("create: tiles cut (thread)");
+    });
+    std::vector<H2DPart> parts(3);
+    parts[0].dst = h->rp; parts[0].src = rs; parts[0].bytes = sizeof(long long) * (size_t)(n + 1);
+    parts[1].dst = h->val; parts[1].src = val; parts[1].bytes = sizeof(double) * (size_t)nnz;
+    parts[2].dst = host_narrow ? (void*)h->col : (void*)tmp;
+    parts[2].src = col;
+    parts[2].bytes = sizeof(long long) * (size_t)nnz;
+    parts[2].conv = host_narrow ? 1 : 0;
+    const int copied = h2d_copy(parts, h->stream, &cmin, &cmax);
+    tr.mark("create: ring copies issued");
     cut.join();
     h->max_row = max_row;
     TRY(copied);
     if (nnz > 0) {
-        k_col64to32<<<(int)std::min<int64_t>((nnz + 255) / 256, 1 << 16), 256, 0, h->stream>>>(
-            tmp, h->col, nnz, (int)h->n_global, bad);
+        if (!host_narrow)
+            k_col64to32<<<(int)std::min<int64_t>((nnz + 255) / 256, 1 << 16), 256, 0, h->stream>>>(
+                tmp, h->col, nnz, (int)h->n_global, bad);
         k_check_rows<<<(int)std::min<int64_t>((n + 255) / 256, 1 << 16), 256, 0, h->stream>>>(
             h->rp, h->col, (int)n, (long long)nnz, bad + 1);
     }
     CK(cudaGetLastError());
     tr.mark("create: copies issued, tiles cut (host)");
     CK(cudaMemcpyAsync(h->bad_host, bad, 2 * sizeof(int), cudaMemcpyDeviceToHost, h->stream));
-    CK(cudaFreeAsync(tmp, h->stream));
+    if (tmp) CK(cudaFreeAsync(tmp, h->stream));
     CK(cudaFreeAsync(bad, h->stream));
     CK(cudaStreamSynchronize(h->stream));
+    if (host_narrow && (cmin < 0 || cmax >= h->n_global)) h->bad_host[0] = 1;
     tr.mark("create: copies + checks done");
     if (!monotone) return fail(MCR_DIMENSION, "rstart must be nondecreasing");
     if (h->bad_host[0]) return fail(MCR_DIMENSION, "column index out of range");

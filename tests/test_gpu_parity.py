@@ -347,6 +347,30 @@ def test_malformed_csr_rejected(gs):
             gs.DeviceMatrix(m, 0)
 
 
+@pytest.mark.parametrize("where,value", [(0, -1), (1, "n"), (1, 2 ** 32 + 5), (None, None)])
+def test_large_csr_columns_narrowed_on_host(gs, where, value):
+    """Pageable columns of >= 1 MiB go over PCIe as int32, narrowed on the host while the ring
+    copies them: the range check still sees every int64 value (2^32 + 5 would wrap to 5)."""
+    from oracle import oracle
+    from paper_1210_6412_b200.sparse import CsrMatrix, DimensionMismatch
+    n = 600_000
+    rs = np.arange(0, 2 * n + 1, 2, dtype=np.int64)
+    col = np.empty(2 * n, dtype=np.int64)
+    col[0::2] = np.arange(n)
+    col[1::2] = np.arange(1, n + 1)
+    col[-2:] = [0, n - 1]
+    val = np.random.default_rng(3).uniform(-2.0, 2.0, 2 * n)
+    if where is not None:
+        k = 2 * (n // 2) + where
+        col[k] = n if value == "n" else value
+        with pytest.raises(DimensionMismatch, match="out of range"):
+            gs.DeviceMatrix(CsrMatrix(n, rs, col, val), 0)
+        return
+    m = CsrMatrix(n, rs, col, val)
+    x = np.random.default_rng(4).uniform(-5.0, 5.0, n)
+    assert np.array_equal(gs.matvec(m, x), oracle.spmv(m, x))
+
+
 def test_matvec_bitwise_random(gs):
     # T/test_sparse.py:133-142 on the device
     from oracle import oracle
