@@ -51,7 +51,7 @@ namespace xd {
 #endif
 constexpr int NT = XD_NT;
 constexpr int NW = NT / 32;
-constexpr int EMAX = 63;  // large n: more products per CTA (C5 20M BiCGStab, E 31 -> 63: 7.13 -> 6.54-6.74 ms per iteration)
+constexpr int EMAX = 79;  // large n: products per CTA (C5 BiCGStab ms per iteration, 20M | 200M: E 31: 7.13 | -, 47: - | 74.6, 63: 6.25 | 68.0, 79: 6.26 | 65.1, 95: 6.91 | 69.8 -- the root's stage runs out of room)
 constexpr unsigned long long MANT = 0x000FFFFFFFFFFFFFull;
 constexpr unsigned long long SGN = 0x8000000000000000ull;
 constexpr int KM_NONE = -4096;
