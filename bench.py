@@ -501,9 +501,9 @@ def run_ours(args):
                      "bound_note": ("gather-bound: 1 random 8-byte x gather per entry; the "
                                     "measured B200 gather floor for C2's 1e7 gathers is "
                                     "~52 us (profiles/r01_gather_microbench.txt). The largest "
-                                    "single kernel of the step (28%, profiles/r02_c2_launches.txt); "
+                                    "single kernel of the step (21% under ncu, profiles/r02_c2_launches.txt); "
                                     "the reference-order dots (k_xdot, 3 launches per BiCGStab "
-                                    "iteration) take 43% together and are bound by dependent adds "
+                                    "iteration) take 35% together and are bound by dependent adds "
                                     "and integer work, not memory (16 B read per product): "
                                     "DESIGN.md 2.1"),
                      "spmv_alone": spmv_alone},
