@@ -50,6 +50,14 @@ namespace xd {
 #define XD_NT 256  // threads per CTA (C2 BiCGStab: 512 -> 27.3 ms, 256 -> 25.2 ms, 128 -> 32.8 ms)
 #endif
 constexpr int NT = XD_NT;
+#ifndef XD_WALK_MAX
+#define XD_WALK_MAX 1  // CTA fold levels whose lanes re-add a stretch a table does not take (above: holes;
+                       // C2 BiCGStab: 0 levels 24.25 ms, 1: 23.70, 2: 23.80, all 3: 25.04)
+#endif
+#ifndef XD_MARGIN
+#define XD_MARGIN 40  // a thread run keeps its partial sums 2^(52 - XD_MARGIN) ulps clear of the binade ends
+                      // (C2 BiCGStab: 36, 40, 44, 48 all 23.68 ms)
+#endif
 constexpr int NW = NT / 32;
 constexpr int EMAX = 79;  // large n: products per CTA (C5 BiCGStab ms per iteration, 20M | 200M: E 31: 7.13 | -, 47: - | 74.6, 63: 6.25 | 68.0, 79: 6.26 | 65.1, 95: 6.91 | 69.8 -- the root's stage runs out of room)
 constexpr unsigned long long MANT = 0x000FFFFFFFFFFFFFull;
@@ -666,7 +674,7 @@ __device__ __forceinline__ Run thread_run(const double* sp, int tl, double pred,
             // the chains model the run only if every partial sum stayed inside the binade, and
             // are worth keeping only if they stayed clear of its ends by more than the prediction's
             // error (4096 ulps); else the thread is summed element by element
-            const double margin = fb((unsigned long long)(e - 40) << 52);
+            const double margin = fb((unsigned long long)(e - XD_MARGIN) << 52);
             const double bot = dadd(fb(((unsigned long long)e << 52) | 1ull), margin);
             const double top = dsub(fb(((unsigned long long)e << 52) | MANT), margin);
             const bool ok = same && (ng ? (-mx0 >= bot && -mn0 <= top && -mx1 >= bot && -mn1 <= top)
@@ -917,7 +925,7 @@ __device__ void tree_fold(const Smem& M, int len, int E, Desc* p, bool walk) {
     for (int s = 1; s < NW; s <<= 1) {
         if (warp < NW / (2 * s)) {
             const int a = 2 * s * warp, b = a + s;
-            compose_pair(M, len, E, p + a, p + b, p + a, a * 32, b * 32, (b + s) * 32, walk && s <= 2);
+            compose_pair(M, len, E, p + a, p + b, p + a, a * 32, b * 32, (b + s) * 32, walk && s <= XD_WALK_MAX);
         }
         __syncthreads();
     }
