@@ -54,11 +54,18 @@ constexpr int NT = XD_NT;
 #define XD_WALK_MAX 1  // CTA fold levels whose lanes re-add a stretch a table does not take (above: holes;
                        // C2 BiCGStab: 0 levels 24.25 ms, 1: 23.70, 2: 23.80, all 3: 25.04)
 #endif
+#ifndef XD_SIM_UNROLL
+#define XD_SIM_UNROLL 12  // C2 BiCGStab: 2: 24.36 ms, 4: 23.74, 8: 23.55, 12: 23.47, 16: 24.07
+#endif
+#ifndef XD_RUN_UNROLL
+#define XD_RUN_UNROLL 4  // 2: 23.82, 8: 23.76
+#endif
 #ifndef XD_MARGIN
 #define XD_MARGIN 40  // a thread run keeps its partial sums 2^(52 - XD_MARGIN) ulps clear of the binade ends
                       // (C2 BiCGStab: 36, 40, 44, 48 all 23.68 ms)
 #endif
 constexpr int NW = NT / 32;
+constexpr int SIM_UNROLL = XD_SIM_UNROLL, RUN_UNROLL = XD_RUN_UNROLL;
 constexpr int EMAX = 79;  // large n: products per CTA (C5 BiCGStab ms per iteration, 20M | 200M: E 31: 7.13 | -, 47: - | 74.6, 63: 6.25 | 68.0, 79: 6.26 | 65.1, 95: 6.91 | 69.8 -- the root's stage runs out of room)
 constexpr unsigned long long MANT = 0x000FFFFFFFFFFFFFull;
 constexpr unsigned long long SGN = 0x8000000000000000ull;
@@ -386,7 +393,7 @@ __device__ __forceinline__ void sim_elems_slow(const double* p, int cnt, double&
     double x = v;
     unsigned lom = (unsigned)__double2hiint(lo) & 0x7fffffffu, him = (unsigned)__double2hiint(hi) & 0x7fffffffu;
     int kmx = km;
-#pragma unroll 4
+#pragma unroll (SIM_UNROLL)
     for (int k = 0; k < cnt; ++k) {
         x = dadd(x, p[k]);
         const unsigned h = (unsigned)__double2hiint(x);
@@ -659,7 +666,7 @@ __device__ __forceinline__ Run thread_run(const double* sp, int tl, double pred,
             // extremes as bit patterns (one sign: they order like the magnitudes; a NaN or a sign
             // change shows up as a different top-12-bit field and fails the binade test below)
             unsigned long long a0 = bt(ref0), z0 = a0, a1 = bt(ref1), z1 = a1;
-#pragma unroll 4
+#pragma unroll (RUN_UNROLL)
             for (int k = 0; k < tl; ++k) {
                 const double p = sp[k];
                 s0 = dadd(s0, p);
