@@ -151,7 +151,7 @@ __device__ __forceinline__ void peer_store(const Vecs& V, int slot, long long g,
 }
 
 enum Epi : int { EPI_Y = 0, EPI_RESID = 1, EPI_JACOBI = 2, EPI_S0 = 3, EPI_V = 4, EPI_T = 5 };
-enum Phase : int { PH_A = 0, PH_C = 1, PH_E = 2 };
+enum Phase : int { PH_A = 0, PH_C = 1, PH_E = 2, PH_EX = 3 };  // PH_EX: E without the tree q.r
 
 template <int EPI> __host__ __device__ constexpr bool epi_checks_stop() { return EPI != EPI_Y && EPI != EPI_RESID; }
 template <int EPI> __host__ __device__ constexpr bool epi_has_max() {

@@ -382,6 +382,10 @@ int bicgstab_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double t
     const bool sh = h->sharded();
     double* p_full = h->vec(V_P);
     double* s_full = h->vec(V_S);
+    // reference-order dots on one device: the E phase needs no q.r partials (MCR_NO_PH_EX=1: the
+    // full phase anyway)
+    static const bool ex_env = std::getenv("MCR_NO_PH_EX") == nullptr;
+    const bool ex = ex_env && h->seqdots && !sh;
     auto body = [&](int64_t* n) {
         launch_phase<PH_A>(h, V, n);               // p = r + beta (p - w v)
         launch_mv<EPI_V>(h, false, p_full, V, n);  // v = M p, q.v -> a
@@ -389,7 +393,8 @@ int bicgstab_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double t
         launch_phase<PH_C>(h, V, n);               // s = r - a v, max|s|
         launch_mv<EPI_T>(h, false, s_full, V, n);  // t = M s, t.t, t.s -> w
         launch_seqdot<SQ_T>(h, V, n);
-        launch_phase<PH_E>(h, V, n);               // x, r updates, q.r -> beta; loop condition
+        if (ex) launch_phase<PH_EX>(h, V, n);      // x, r updates (q.r: the next launch)
+        else launch_phase<PH_E>(h, V, n);          // x, r updates, q.r -> beta; loop condition
         launch_seqdot<SQ_E>(h, V, n);
     };
     // From the second BiCGStab solve of a handle the loop is the graph from the start. On the
@@ -476,7 +481,8 @@ int bicgstab_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double t
             if (sh && h->seqdots) TRY(allgather_full(h, h->vec(V_T)));
             launch_seqdot<SQ_T>(h, V, &launched);
             if (sh) TRY(exchange_point<FIN_T>(h, nullptr, &launched));
-            launch_phase<PH_E>(h, V, &launched);               // x, r updates, q.r -> beta
+            if (ex) launch_phase<PH_EX>(h, V, &launched);      // x, r updates
+            else launch_phase<PH_E>(h, V, &launched);          // x, r updates, q.r -> beta
             if (sh && h->seqdots) TRY(allgather_full(h, h->vec(V_R)));
             launch_seqdot<SQ_E>(h, V, &launched);
             if (sh) TRY(exchange_point<FIN_E>(h, nullptr, &launched));

@@ -71,6 +71,31 @@ __global__ void __launch_bounds__(CHUNK_NT) k_phase(Vecs V, int n, SolveState* s
         if (V.peers) __threadfence_system();
         mb = group_max<CHUNK_NT / 32, 0>(mb, s_redu);
         if (threadIdx.x == 0 && mb && !stop) atomicMax(&st->maxbits, mb);
+    } else if constexpr (PH == PH_EX) {
+        // E with the reference-order dots on one device: the x and r updates alone (q.r is
+        // k_xdot's), A/C-sized chunks, no partials; a stopped solve ends the graph loop here
+        const double a = st->a, w = st->w;
+        const int stop = st->stop;
+        double xv[CHUNK_PER], p[CHUNK_PER], s[CHUNK_PER], t[CHUNK_PER];
+#pragma unroll
+        for (int u = 0; u < CHUNK_PER; ++u) {
+            const int i = base + u * CHUNK_NT;
+            if (i < n) {
+                xv[u] = V.x[i]; p[u] = __ldcs(V.p + i); s[u] = __ldcs(V.s + i); t[u] = __ldcs(V.t + i);
+            }
+        }
+        const long long keep = stop ? -1ll : 0ll;  // bit select, not a branch (see above)
+#pragma unroll
+        for (int u = 0; u < CHUNK_PER; ++u) {
+            const int i = base + u * CHUNK_NT;
+            if (i < n) {
+                const double xn = dadd(dadd(xv[u], dmul(a, p[u])), dmul(w, s[u]));  // x + a p + w s
+                V.x[i] = __longlong_as_double((__double_as_longlong(xn) & ~keep) |
+                                              (__double_as_longlong(xv[u]) & keep));
+                V.r[i] = dsub(s[u], dmul(w, t[u]));                               // r = s - w t
+            }
+        }
+        if (stop && blockIdx.x == 0 && threadIdx.x == 0) graph_continue(st);  // stopped earlier
     } else {
         const double a = st->a, w = st->w;
         const int stop = st->stop;
