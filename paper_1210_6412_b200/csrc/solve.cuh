@@ -386,12 +386,24 @@ int bicgstab_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double t
     // full phase anyway)
     static const bool ex_env = std::getenv("MCR_NO_PH_EX") == nullptr;
     const bool ex = ex_env && h->seqdots && !sh;
+    // ... nor do the two SpMVs: plain y = M x stores into v and t
+    Vecs Vv = V, Vt = V;
+    Vv.y = V.v;
+    Vt.y = V.t;
+    auto mv_v = [&](int64_t* n) {  // v = M p (q.v -> a unless the dots are k_xdot's)
+        if (ex) launch_mv<EPI_Y>(h, false, p_full, Vv, n);
+        else launch_mv<EPI_V>(h, false, p_full, V, n);
+    };
+    auto mv_t = [&](int64_t* n) {  // t = M s (t.t, t.s -> w unless the dots are k_xdot's)
+        if (ex) launch_mv<EPI_Y>(h, false, s_full, Vt, n);
+        else launch_mv<EPI_T>(h, false, s_full, V, n);
+    };
     auto body = [&](int64_t* n) {
         launch_phase<PH_A>(h, V, n);               // p = r + beta (p - w v)
-        launch_mv<EPI_V>(h, false, p_full, V, n);  // v = M p, q.v -> a
+        mv_v(n);                                   // v = M p, q.v -> a
         launch_seqdot<SQ_V>(h, V, n);
         launch_phase<PH_C>(h, V, n);               // s = r - a v, max|s|
-        launch_mv<EPI_T>(h, false, s_full, V, n);  // t = M s, t.t, t.s -> w
+        mv_t(n);                                   // t = M s, t.t, t.s -> w
         launch_seqdot<SQ_T>(h, V, n);
         if (ex) launch_phase<PH_EX>(h, V, n);      // x, r updates (q.r: the next launch)
         else launch_phase<PH_E>(h, V, n);          // x, r updates, q.r -> beta; loop condition
@@ -471,13 +483,13 @@ int bicgstab_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double t
         for (int i = 0; i < k; ++i) {
             launch_phase<PH_A>(h, V, &launched);               // p = r + beta (p - w v)
             if (sh) TRY(h->p2p ? p2p_barrier(h) : allgather_full(h, p_full));
-            launch_mv<EPI_V>(h, false, p_full, V, &launched);  // v = M p, q.v -> a
+            mv_v(&launched);                                   // v = M p, q.v -> a
             if (sh && h->seqdots) TRY(allgather_full(h, h->vec(V_V)));
             launch_seqdot<SQ_V>(h, V, &launched);
             if (sh) TRY(exchange_point<FIN_V>(h, nullptr, &launched));
             launch_phase<PH_C>(h, V, &launched);               // s = r - a v, max|s|
             if (sh) TRY(h->p2p ? p2p_barrier(h) : allgather_full(h, s_full));
-            launch_mv<EPI_T>(h, false, s_full, V, &launched);  // t = M s, t.t, t.s -> w
+            mv_t(&launched);                                   // t = M s, t.t, t.s -> w
             if (sh && h->seqdots) TRY(allgather_full(h, h->vec(V_T)));
             launch_seqdot<SQ_T>(h, V, &launched);
             if (sh) TRY(exchange_point<FIN_T>(h, nullptr, &launched));
