@@ -386,16 +386,19 @@ int bicgstab_impl(mcr_matrix* h, const double* d_b, const double* d_x0, double t
     // full phase anyway)
     static const bool ex_env = std::getenv("MCR_NO_PH_EX") == nullptr;
     const bool ex = ex_env && h->seqdots && !sh;
-    // ... nor do the two SpMVs: plain y = M x stores into v and t
+    // ... nor do the two SpMVs: plain y = M x stores into v and t (the tiled CSR kernel only:
+    // the dense, staged and SELL kernels measured slower with the plain epilogue -- C3 BiCGStab
+    // 4.2 -> 5.9 ms, C5 2-4%)
+    const bool plain_mv = ex && h->storage != MCR_STORAGE_DENSE && !h->use_staged && !h->use_sell;
     Vecs Vv = V, Vt = V;
     Vv.y = V.v;
     Vt.y = V.t;
     auto mv_v = [&](int64_t* n) {  // v = M p (q.v -> a unless the dots are k_xdot's)
-        if (ex) launch_mv<EPI_Y>(h, false, p_full, Vv, n);
+        if (plain_mv) launch_mv<EPI_Y>(h, false, p_full, Vv, n);
         else launch_mv<EPI_V>(h, false, p_full, V, n);
     };
     auto mv_t = [&](int64_t* n) {  // t = M s (t.t, t.s -> w unless the dots are k_xdot's)
-        if (ex) launch_mv<EPI_Y>(h, false, s_full, Vt, n);
+        if (plain_mv) launch_mv<EPI_Y>(h, false, s_full, Vt, n);
         else launch_mv<EPI_T>(h, false, s_full, V, n);
     };
     auto body = [&](int64_t* n) {
